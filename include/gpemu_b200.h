@@ -1,0 +1,147 @@
+/*
+ * gpemu_b200.h -- C-ABI of the B200-native gpemu hot path.
+ *
+ * Plain pointers and sizes only (no torch / CUDA types in the signatures).
+ * Every call returns an int status (gpemu_status); gpemu_last_error() gives a
+ * thread-local message. Host buffers are caller-allocated; ctx / plan / model
+ * are opaque handles owned by the library. There is NO CPU fallback: every
+ * compute entry point runs sm_100a kernels and fails with GPEMU_CUDA when no
+ * usable device is present.
+ *
+ * Reference interface each entry point replaces (paths relative to
+ * /root/reference/proj/include/gpemu/):
+ */
+#ifndef GPEMU_B200_H
+#define GPEMU_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:9-36 exception hierarchy as status codes */
+typedef enum {
+  GPEMU_OK = 0,
+  GPEMU_VALIDATION = 1,  /* ValidationError */
+  GPEMU_NOT_PD = 2,      /* NotPositiveDefiniteError */
+  GPEMU_FIT = 3,         /* FitError */
+  GPEMU_CONFIG = 4,      /* ConfigError */
+  GPEMU_NONFINITE = 5,   /* Error("... non-finite correlation value") */
+  GPEMU_CUDA = 6,        /* device / driver failure (Error) */
+  GPEMU_ERROR = 7        /* any other Error */
+} gpemu_status;
+
+/* Per-candidate status word written by the device for every batch slot. */
+typedef enum {
+  GPEMU_SLOT_OK = 0,
+  GPEMU_SLOT_NOT_PD = 1,    /* ladder exhausted -> neg2 = +inf (likelihood.hpp:115-119) */
+  GPEMU_SLOT_NONFINITE = 2, /* non-finite R entry (correlation.hpp:222) */
+  GPEMU_SLOT_DEGENERATE = 3 /* vtv <= 0 -> +inf (likelihood.hpp:127) */
+} gpemu_slot_status;
+
+typedef struct gpemu_ctx gpemu_ctx;
+typedef struct gpemu_plan gpemu_plan;
+typedef struct gpemu_model gpemu_model;
+
+/* Cholesky engine selection (gpemu_ctx_set_engine). */
+typedef enum {
+  GPEMU_ENGINE_DAG = 0,    /* persistent tile-DAG, DMMA trailing updates (default) */
+  GPEMU_ENGINE_SIMPLE = 1  /* one CTA per candidate, unblocked; validation engine */
+} gpemu_engine;
+
+const char* gpemu_last_error(void);
+const char* gpemu_version(void);
+
+/* -- context: one device, one stream ------------------------------------ */
+int gpemu_ctx_create(int device, gpemu_ctx** out);
+int gpemu_ctx_destroy(gpemu_ctx* ctx);
+/* Use an external cudaStream_t (passed as void*); NULL restores the ctx's own. */
+int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream);
+int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine);
+/* Number of kernels this ctx has launched so far (bench accounting). */
+uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx);
+
+/* -- correlation.hpp ------------------------------------------------------ */
+/* build_corr_matrix (correlation.hpp:99-146) / CorrelationPlan::build_into (:187-223):
+ * R (n x n row-major, both triangles written) for one theta. */
+int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
+                     double p, double nugget, double* R_out);
+/* corr_vector (correlation.hpp:67-91): r_i for one test point, no nugget. */
+int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size_t n, size_t d,
+                      const double* theta, double p, double* r_out);
+
+/* -- backend.hpp ---------------------------------------------------------- */
+/* Backend::factorize_into (backend.hpp:102-120): Cholesky of R + jitter I with the
+ * kJitterLadder escalation. L_out: n x n row-major, lower triangle meaningful,
+ * strict upper zeroed. Returns GPEMU_NOT_PD when the ladder is exhausted. */
+int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
+                    double* jitter_used);
+/* Backend::solve_lower_into (:129-140) / solve_upper_into (:143-153). */
+int gpemu_solve_lower(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
+int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
+
+/* -- likelihood.hpp ------------------------------------------------------- */
+/* ProfileEvaluator ctor (likelihood.hpp:77-91): uploads X, y, builds the
+ * |dx|^p table on the device. max_batch bounds the candidates per eval call. */
+int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
+                      double p, double nugget, size_t max_batch, gpemu_plan** out);
+int gpemu_plan_destroy(gpemu_plan* plan);
+size_t gpemu_plan_device_bytes(const gpemu_plan* plan);
+
+/* ProfileEvaluator::eval (likelihood.hpp:108-141), batched over B independent
+ * thetas (host arrays). Any output pointer may be NULL. Per-slot results are
+ * independent of B and of the slot index (batch invariance). */
+int gpemu_eval_batch(gpemu_plan* plan, const double* theta, size_t B, double* neg2, double* mu,
+                     double* sigma2, double* jitter, double* log_det, int* slot_status);
+
+/* Same on device memory: d_theta (B x d doubles), d_out (B x 8 doubles:
+ * neg2, mu, sigma2, jitter, log_det, status, utu, vtv). Synchronises only to
+ * run the jitter ladder (one B-int status read per ladder step). */
+int gpemu_eval_batch_device(gpemu_plan* plan, const double* d_theta, size_t B, double* d_out);
+
+/* ProfileEvaluator::last_factor (likelihood.hpp:103) of a batch slot of the most
+ * recent eval: L (n x n row-major, strict upper zero). */
+int gpemu_plan_last_factor(gpemu_plan* plan, size_t slot, double* L_out, double* log_det,
+                           double* jitter_used);
+
+/* ---- optimizer.hpp / likelihood.hpp fit ------------------------------- */
+typedef struct {
+  int population;       /* GaConfig::population (100) */
+  int generations;      /* GaConfig::generations (20) */
+  double crossover_rate;/* 0.9 */
+  double mutation_sigma;/* 0.15 */
+  double mutation_prob; /* 0 -> 1/d */
+  int elitism;          /* 1 */
+} gpemu_ga_config;
+
+typedef struct {
+  double neg2_log_lik, mu_hat, sigma2_hat, jitter_max;
+  uint64_t r_builds, factorizations, triangular_solves; /* Ledger (backend.hpp:26-49) */
+} gpemu_fit_result;
+
+/* fit_gp_detailed (likelihood.hpp:243-303): GA over log10(theta) in [lo, hi]
+ * with one device batch per generation; the stash keeps the earliest best
+ * (generation, slot) exactly like the sequential reference. theta_hat (d),
+ * alpha (n), trace_best (generations), trace_genes (generations*d) may be NULL.
+ * model_out (nullable) receives a device-resident GpModel for gpemu_predict. */
+int gpemu_fit(gpemu_plan* plan, const double* lo, const double* hi, const gpemu_ga_config* ga,
+              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
+              double* trace_best, double* trace_genes, gpemu_model** model_out);
+
+/* model_at_theta (likelihood.hpp:216-237). scalars: neg2, mu, sigma2, jitter. */
+int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,
+                         double* scalars, double* alpha);
+int gpemu_model_destroy(gpemu_model* model);
+
+/* ---- predictor.hpp ------------------------------------------------------ */
+/* predict (predictor.hpp:20-50): yhat_j = mu + r(x_j)' alpha; mse (nullable) is the
+ * kriging MSE sigma2 (1 - w'w + (1 - v'w)^2 / v'v), w = L^-1 r, v = L^-1 1
+ * (no reference implementation). Validates the unit cube. */
+int gpemu_predict(gpemu_model* model, const double* Xtest, size_t N, double* yhat, double* mse);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPEMU_B200_H */

@@ -231,9 +231,9 @@ class Oracle:
 class RefLib:
     """The reference's own headers behind ref_shim.cpp (oracle/_ref)."""
 
-    def __init__(self, fast: bool = False):
+    def __init__(self, fast: bool = False, path: str | None = None):
         name = "libgpemu_ref_fast.so" if fast else "libgpemu_ref.so"
-        path = os.path.join(HERE, "_ref", name)
+        path = path or os.path.join(HERE, "_ref", name)
         if not os.path.exists(path):
             raise FileNotFoundError(path)
         L = C.CDLL(path)

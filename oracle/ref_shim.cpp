@@ -37,17 +37,19 @@ Matrix<double> to_matrix(const double* p, std::size_t r, std::size_t c) {
   }               \
   catch (const std::exception& e) { return map_error(e); }
 
+#define REF_API __attribute__((visibility("default")))
+
 extern "C" {
 
-const char* ref_last_error() { return g_err.c_str(); }
+REF_API const char* ref_last_error() { return g_err.c_str(); }
 
-std::uint64_t ref_derive_seed2(std::uint64_t b, std::uint64_t a) { return detail::derive_seed(b, a); }
-std::uint64_t ref_derive_seed3(std::uint64_t b, std::uint64_t a, std::uint64_t c) {
+REF_API std::uint64_t ref_derive_seed2(std::uint64_t b, std::uint64_t a) { return detail::derive_seed(b, a); }
+REF_API std::uint64_t ref_derive_seed3(std::uint64_t b, std::uint64_t a, std::uint64_t c) {
   return detail::derive_seed(b, a, c);
 }
 
 // kind 0: next_u64 (as double bits), 1: uniform01, 2: normal, 3: below(arg)
-void ref_rng_draws(std::uint64_t seed, int kind, std::uint64_t arg, std::size_t count, double* out) {
+REF_API void ref_rng_draws(std::uint64_t seed, int kind, std::uint64_t arg, std::size_t count, double* out) {
   detail::Rng rng(seed);
   for (std::size_t i = 0; i < count; ++i) {
     if (kind == 0) {
@@ -63,7 +65,7 @@ void ref_rng_draws(std::uint64_t seed, int kind, std::uint64_t arg, std::size_t 
   }
 }
 
-int ref_maximin_lhd(std::size_t n, std::size_t d, std::uint64_t seed, std::size_t budget, double* X) {
+REF_API int ref_maximin_lhd(std::size_t n, std::size_t d, std::uint64_t seed, std::size_t budget, double* X) {
   REF_TRY
   const auto m = maximin_lhd(DesignSpec{n, d, seed, budget});
   std::memcpy(X, m.data(), n * d * sizeof(double));
@@ -71,10 +73,10 @@ int ref_maximin_lhd(std::size_t n, std::size_t d, std::uint64_t seed, std::size_
   REF_CATCH
 }
 
-double ref_goldstein_price_log(const double* x) { return goldstein_price_log(std::span<const double>(x, 2)); }
-double ref_hartman6(const double* x) { return hartman6(std::span<const double>(x, 6)); }
+REF_API double ref_goldstein_price_log(const double* x) { return goldstein_price_log(std::span<const double>(x, 2)); }
+REF_API double ref_hartman6(const double* x) { return hartman6(std::span<const double>(x, 6)); }
 
-void ref_lhs_population(const double* lo, const double* hi, std::size_t d, int count,
+REF_API void ref_lhs_population(const double* lo, const double* hi, std::size_t d, int count,
                         std::uint64_t seed, double* pop) {
   std::vector<std::pair<double, double>> b(d);
   for (std::size_t k = 0; k < d; ++k) b[k] = {lo[k], hi[k]};
@@ -84,7 +86,7 @@ void ref_lhs_population(const double* lo, const double* hi, std::size_t d, int c
     for (std::size_t k = 0; k < d; ++k) pop[i * d + k] = P[i][k];
 }
 
-int ref_build_corr(const double* X, std::size_t n, std::size_t d, const double* theta, double p,
+REF_API int ref_build_corr(const double* X, std::size_t n, std::size_t d, const double* theta, double p,
                    double nugget, double* R) {
   REF_TRY
   const auto r = build_corr_matrix(to_matrix(X, n, d),
@@ -94,7 +96,7 @@ int ref_build_corr(const double* X, std::size_t n, std::size_t d, const double* 
   REF_CATCH
 }
 
-int ref_plan_build(const double* X, std::size_t n, std::size_t d, const double* theta, double p,
+REF_API int ref_plan_build(const double* X, std::size_t n, std::size_t d, const double* theta, double p,
                    double nugget, unsigned threads, double* R) {
   REF_TRY
   const auto x = to_matrix(X, n, d);
@@ -107,7 +109,7 @@ int ref_plan_build(const double* X, std::size_t n, std::size_t d, const double* 
   REF_CATCH
 }
 
-int ref_corr_vector(const double* xstar, const double* X, std::size_t n, std::size_t d,
+REF_API int ref_corr_vector(const double* xstar, const double* X, std::size_t n, std::size_t d,
                     const double* theta, double p, double* r) {
   REF_TRY
   const auto v = corr_vector<double>(std::span<const double>(xstar, d), to_matrix(X, n, d),
@@ -117,7 +119,7 @@ int ref_corr_vector(const double* xstar, const double* X, std::size_t n, std::si
   REF_CATCH
 }
 
-int ref_factorize(const double* R, std::size_t n, const char* backend, unsigned threads, double* L,
+REF_API int ref_factorize(const double* R, std::size_t n, const char* backend, unsigned threads, double* L,
                   double* log_det, double* jitter) {
   REF_TRY
   auto be = make_backend<double>(backend, threads);
@@ -130,7 +132,7 @@ int ref_factorize(const double* R, std::size_t n, const char* backend, unsigned 
   REF_CATCH
 }
 
-int ref_solve(const double* L, std::size_t n, const double* b, int upper, double* x) {
+REF_API int ref_solve(const double* L, std::size_t n, const double* b, int upper, double* x) {
   REF_TRY
   auto be = make_backend<double>("reference");
   CorrelationFactor<double> f;
@@ -146,7 +148,7 @@ int ref_solve(const double* L, std::size_t n, const double* b, int upper, double
 
 // ProfileEvaluator::eval over B thetas (one evaluator: one plan, as in the fit).
 // log_det may be NULL; it is read from last_factor() after each finite eval.
-int ref_eval_batch(const double* X, const double* y, std::size_t n, std::size_t d, double p,
+REF_API int ref_eval_batch(const double* X, const double* y, std::size_t n, std::size_t d, double p,
                    double nugget, const double* thetas, std::size_t B, const char* backend,
                    unsigned threads, double* neg2, double* mu, double* sigma2, double* jitter,
                    double* log_det) {
@@ -167,7 +169,7 @@ int ref_eval_batch(const double* X, const double* y, std::size_t n, std::size_t 
 }
 
 // fit_gp_detailed with the default GaConfig except population/generations.
-int ref_fit(const double* X, const double* y, std::size_t n, std::size_t d, double p, double nugget,
+REF_API int ref_fit(const double* X, const double* y, std::size_t n, std::size_t d, double p, double nugget,
             const double* lo, const double* hi, int population, int generations, std::uint64_t seed,
             const char* backend, unsigned threads, double* theta_hat, double* scalars /*neg2,mu,sigma2,jitter_max*/,
             double* alpha, double* trace_best, double* trace_genes) {
@@ -199,7 +201,7 @@ int ref_fit(const double* X, const double* y, std::size_t n, std::size_t d, doub
 }
 
 // model_at_theta + predict (predictor.hpp:20-50).
-int ref_model_predict(const double* X, const double* y, std::size_t n, std::size_t d,
+REF_API int ref_model_predict(const double* X, const double* y, std::size_t n, std::size_t d,
                       const double* theta, double p, double nugget, const char* backend,
                       unsigned threads, const double* Xtest, std::size_t N, double* yhat,
                       double* scalars /*neg2,mu,sigma2,jitter*/, double* alpha) {

@@ -1,0 +1,879 @@
+// capi.cu -- host runtime behind include/gpemu_b200.h.
+//
+// Owns device memory, the jitter-ladder batch executor, the batched GA driver
+// and the C-ABI. Mirrors the reference's host logic (paths relative to
+// /root/reference/proj/include/gpemu/):
+//   Hyperparameters::validate   core.hpp:76-83
+//   FitConfig::bounds_for       core.hpp:114-123
+//   Backend::factorize_into     backend.hpp:102-120 (ladder; one factorization in the Ledger)
+//   ProfileEvaluator            likelihood.hpp:74-158
+//   ga_minimize                 optimizer.hpp:93-187 (candidate sequence reproduced exactly;
+//                               each generation's population is ONE device batch)
+//   fit_gp_detailed             likelihood.hpp:243-303 (stash: strict <, earliest slot wins)
+//   model_at_theta / predict    likelihood.hpp:216-237, predictor.hpp:20-50
+// There is no CPU fallback: every numeric result comes from the sm_100a kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/gpemu_b200.h"
+#include "kernels.h"
+#include "layout.cuh"
+
+using namespace gpemu_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int set_error(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+struct CudaError {
+  std::string msg;
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+constexpr double kLadder[6] = {0.0, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4};  // backend.hpp:77
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t count = 0;
+  void alloc(size_t c) {
+    free();
+    if (c == 0) c = 1;
+    ck(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
+    count = c;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    count = 0;
+  }
+  ~DevBuf() { free(); }
+};
+
+// splitmix64 seed derivation (rng.hpp:12-25).
+uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ull;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+uint64_t derive_seed(uint64_t base) { return mix64(base); }
+uint64_t derive_seed(uint64_t base, uint64_t a) { return derive_seed(mix64(base ^ mix64(a))); }
+uint64_t derive_seed(uint64_t base, uint64_t a, uint64_t b) {
+  return derive_seed(mix64(base ^ mix64(a)), b);
+}
+
+// Rng mappings of rng.hpp:29-58 over std::mt19937_64.
+struct Rng {
+  std::mt19937_64 eng;
+  explicit Rng(uint64_t seed) : eng(seed) {}
+  double uniform01() { return static_cast<double>(eng() >> 11) * 0x1.0p-53; }
+  double uniform01_open_low() { return static_cast<double>((eng() >> 11) + 1) * 0x1.0p-53; }
+  uint64_t below(uint64_t n) {
+    return static_cast<uint64_t>((static_cast<__uint128_t>(eng()) * n) >> 64);
+  }
+  double normal() {
+    const double u1 = uniform01_open_low();
+    const double u2 = uniform01();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * 3.141592653589793 * u2);
+  }
+};
+
+int validate_params(const double* theta, size_t d, double p, double nugget) {
+  for (size_t k = 0; k < d; ++k) {
+    if (!(theta[k] >= 0.0) || !std::isfinite(theta[k]))
+      return set_error(GPEMU_VALIDATION, "Hyperparameters: theta entries must be finite and nonnegative");
+  }
+  if (!(p > 0.0) || !(p <= 2.0)) return set_error(GPEMU_VALIDATION, "Hyperparameters: p must be in (0, 2]");
+  if (!(nugget >= 0.0) || !std::isfinite(nugget))
+    return set_error(GPEMU_VALIDATION, "Hyperparameters: nugget must be finite and nonnegative");
+  return GPEMU_OK;
+}
+
+int validate_unit_cube(const double* X, size_t rows, size_t d, const char* who) {
+  for (size_t i = 0; i < rows * d; ++i) {
+    const double x = X[i];
+    if (!std::isfinite(x)) return set_error(GPEMU_VALIDATION, "%s: non-finite input coordinate", who);
+    if (x < -1e-12 || x > 1.0 + 1e-12)
+      return set_error(GPEMU_VALIDATION, "%s: coordinate %g outside the unit cube at row %zu", who, x, i / d);
+  }
+  return GPEMU_OK;
+}
+
+}  // namespace
+
+struct gpemu_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int engine = GPEMU_ENGINE_DAG;
+  int num_sms = 148;
+  uint64_t launches = 0;
+};
+
+struct gpemu_plan {
+  gpemu_ctx* ctx = nullptr;
+  int n = 0, d = 0, NT = 0, Npad = 0;
+  double p = 1.95, nugget = 0.0;
+  size_t max_batch = 0, nslots = 0;  // nslots = max_batch + 1 (stash slot)
+  size_t slot_stride = 0;
+  int epoch = 0;
+  DevBuf<double> X, y, table, factors, borders, theta, jitter, out;
+  DevBuf<int> status, slots, flags, counter, error;
+  std::vector<double> h_jitter;
+  std::vector<int> h_slots, h_status_all;
+  std::vector<double> h_out;
+  size_t last_B = 0;
+  std::vector<int> last_ladder;  // ladder step per slot of the last batch (-1: failed)
+  uint64_t r_builds = 0, factorizations = 0, solves = 0;
+};
+
+struct gpemu_model {
+  gpemu_ctx* ctx = nullptr;
+  int n = 0, d = 0, NT = 0;
+  double p = 1.95, mu = 0.0, sigma2 = 0.0, vtv = 0.0, neg2 = 0.0, jitter = 0.0;
+  std::vector<double> theta;
+  DevBuf<double> X, theta_d, alpha, tiles, v;
+};
+
+namespace {
+
+void run_chol(gpemu_plan* pl, int nact) {
+  DagLaunch a;
+  a.factors = pl->factors.p;
+  a.borders = pl->borders.p;
+  a.slot_stride = pl->slot_stride;
+  a.n = pl->n;
+  a.NT = pl->NT;
+  a.slots = pl->slots.p;
+  a.nslots = nact;
+  a.counter = pl->counter.p;
+  a.flags = pl->flags.p;
+  a.epoch = ++pl->epoch;
+  a.status = pl->status.p;
+  a.error = pl->error.p;
+  if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
+    launch_chol_simple(a, pl->ctx->stream);
+  } else {
+    launch_chol_dag(a, pl->ctx->num_sms, pl->ctx->stream);
+  }
+  pl->ctx->launches += 1;
+}
+
+// Evaluates slots [0, B) whose thetas are already in pl->theta; runs the jitter
+// ladder (backend.hpp:105-119) on the device, re-assembling R only for the
+// candidates whose factorization failed. Leaves records in pl->out.
+int run_batch(gpemu_plan* pl, size_t B) {
+  cudaStream_t s = pl->ctx->stream;
+  pl->last_B = B;
+  pl->last_ladder.assign(B, -1);
+  std::vector<int> active(B);
+  std::iota(active.begin(), active.end(), 0);
+  for (size_t i = 0; i < B; ++i) pl->h_jitter[i] = 0.0;
+  ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), B * sizeof(double), cudaMemcpyHostToDevice, s),
+     "H2D jitter");
+  for (int step = 0; step < 6 && !active.empty(); ++step) {
+    const int nact = (int)active.size();
+    if (step > 0) {
+      for (int q = 0; q < nact; ++q) pl->h_jitter[active[q]] = kLadder[step];
+      ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), B * sizeof(double),
+                         cudaMemcpyHostToDevice, s),
+         "H2D jitter");
+    }
+    std::copy(active.begin(), active.end(), pl->h_slots.begin());
+    ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), nact * sizeof(int), cudaMemcpyHostToDevice, s),
+       "H2D slots");
+    launch_assemble(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
+                    pl->slots.p, nact, pl->jitter.p, pl->factors.p, pl->slot_stride,
+                    pl->borders.p, pl->status.p, s);
+    run_chol(pl, nact);
+    launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
+                    pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+    pl->ctx->launches += 4;
+    ck(cudaGetLastError(), "kernel launch");
+    ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, B * sizeof(int), cudaMemcpyDeviceToHost, s),
+       "D2H status");
+    ck(cudaStreamSynchronize(s), "batch");
+    std::vector<int> failed;
+    for (int q = 0; q < nact; ++q) {
+      const int slot = active[q];
+      const int st = pl->h_status_all[slot];
+      if (st == 2) return set_error(GPEMU_NONFINITE, "CorrelationPlan: non-finite correlation value");
+      if (st == 1) {
+        failed.push_back(slot);
+      } else {
+        pl->last_ladder[slot] = step;
+      }
+    }
+    active.swap(failed);
+  }
+  int err = 0;
+  ck(cudaMemcpy(&err, pl->error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H error");
+  if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
+  pl->r_builds += B;
+  pl->factorizations += B;
+  pl->solves += 2 * B;
+  return GPEMU_OK;
+}
+
+int download_records(gpemu_plan* pl, size_t B) {
+  ck(cudaMemcpyAsync(pl->h_out.data(), pl->out.p, B * REC_SIZE * sizeof(double),
+                     cudaMemcpyDeviceToHost, pl->ctx->stream),
+     "D2H out");
+  ck(cudaStreamSynchronize(pl->ctx->stream), "D2H out");
+  return GPEMU_OK;
+}
+
+// alpha = (R + jI)^-1 (y - mu 1) on the factor of `slot` (solve_full, backend.hpp:163-169).
+void solve_alpha(gpemu_plan* pl, int slot, double mu, double* d_alpha) {
+  cudaStream_t s = pl->ctx->stream;
+  std::vector<double> hy(pl->n);
+  // rhs is formed on the host from y (an O(n) subtraction, as likelihood.hpp:288).
+  ck(cudaMemcpy(hy.data(), pl->y.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H y");
+  for (int i = 0; i < pl->n; ++i) hy[i] = hy[i] - mu;
+  DevBuf<double> rhs, u;
+  rhs.alloc(pl->n);
+  u.alloc(pl->n);
+  ck(cudaMemcpy(rhs.p, hy.data(), pl->n * sizeof(double), cudaMemcpyHostToDevice), "H2D rhs");
+  const double* tiles = pl->factors.p + (size_t)slot * pl->slot_stride;
+  launch_tri_solve(tiles, pl->n, pl->NT, rhs.p, u.p, 0, s);
+  launch_tri_solve(tiles, pl->n, pl->NT, u.p, d_alpha, 1, s);
+  pl->ctx->launches += 2;
+  ck(cudaStreamSynchronize(s), "solve_alpha");
+  pl->solves += 2;
+}
+
+gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const double* rec) {
+  auto* m = new gpemu_model();
+  m->ctx = pl->ctx;
+  m->n = pl->n;
+  m->d = pl->d;
+  m->NT = pl->NT;
+  m->p = pl->p;
+  m->neg2 = rec[REC_NEG2];
+  m->mu = rec[REC_MU];
+  m->sigma2 = rec[REC_SIGMA2];
+  m->vtv = rec[REC_VTV];
+  m->jitter = rec[REC_JITTER];
+  m->theta.assign(theta, theta + pl->d);
+  cudaStream_t s = pl->ctx->stream;
+  m->X.alloc((size_t)pl->n * pl->d);
+  m->theta_d.alloc(pl->d);
+  m->alpha.alloc(pl->n);
+  m->tiles.alloc(pl->slot_stride);
+  m->v.alloc(pl->Npad);
+  ck(cudaMemcpyAsync(m->X.p, pl->X.p, (size_t)pl->n * pl->d * sizeof(double), cudaMemcpyDeviceToDevice, s), "model X");
+  ck(cudaMemcpyAsync(m->theta_d.p, theta, pl->d * sizeof(double), cudaMemcpyHostToDevice, s), "model theta");
+  ck(cudaMemcpyAsync(m->tiles.p, pl->factors.p + (size_t)slot * pl->slot_stride,
+                     pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
+     "model tiles");
+  ck(cudaMemcpyAsync(m->v.p, pl->borders.p + (size_t)slot * 2 * pl->Npad + pl->Npad,
+                     pl->Npad * sizeof(double), cudaMemcpyDeviceToDevice, s),
+     "model v");
+  solve_alpha(pl, slot, m->mu, m->alpha.p);
+  return m;
+}
+
+}  // namespace
+
+#define GPEMU_GUARD_BEGIN try {
+#define GPEMU_GUARD_END                                        \
+  }                                                            \
+  catch (const CudaError& e) {                                 \
+    return set_error(GPEMU_CUDA, "%s", e.msg.c_str());        \
+  }                                                            \
+  catch (const std::bad_alloc&) {                              \
+    return set_error(GPEMU_ERROR, "host allocation failed");   \
+  }
+
+extern "C" {
+
+const char* gpemu_last_error(void) { return g_last_error.c_str(); }
+const char* gpemu_version(void) { return "gpemu_b200 0.1 (sm_100a)"; }
+
+int gpemu_ctx_create(int device, gpemu_ctx** out) {
+  GPEMU_GUARD_BEGIN
+  if (!out) return set_error(GPEMU_VALIDATION, "ctx_create: null out");
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    return set_error(GPEMU_CUDA, "no CUDA device available (the B200 engine has no CPU fallback)");
+  if (device < 0 || device >= count) return set_error(GPEMU_CONFIG, "ctx_create: bad device %d", device);
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major < 10)
+    return set_error(GPEMU_CUDA, "device %s (sm_%d%d) is not Blackwell sm_100", prop.name, prop.major, prop.minor);
+  auto* c = new gpemu_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+  c->stream = c->own;
+  *out = c;
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_ctx_destroy(gpemu_ctx* ctx) {
+  if (!ctx) return GPEMU_OK;
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+  return GPEMU_OK;
+}
+
+int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream) {
+  if (!ctx) return set_error(GPEMU_VALIDATION, "null ctx");
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return GPEMU_OK;
+}
+
+int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine) {
+  if (!ctx) return set_error(GPEMU_VALIDATION, "null ctx");
+  if (engine != GPEMU_ENGINE_DAG && engine != GPEMU_ENGINE_SIMPLE)
+    return set_error(GPEMU_CONFIG, "unknown engine %d", engine);
+  ctx->engine = engine;
+  return GPEMU_OK;
+}
+
+uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------------------
+int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
+                     double p, double nugget, double* R_out) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !X || !theta || !R_out) return set_error(GPEMU_VALIDATION, "build_corr: null argument");
+  int rc = validate_params(theta, d, p, nugget);
+  if (rc) return rc;
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  DevBuf<double> dX, dT, dR;
+  DevBuf<int> bad;
+  dX.alloc(n * d);
+  dT.alloc(d);
+  dR.alloc(n * n);
+  bad.alloc(1);
+  cudaStream_t s = ctx->stream;
+  ck(cudaMemcpyAsync(dX.p, X, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D X");
+  ck(cudaMemcpyAsync(dT.p, theta, d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+  ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
+  if (n > 0) launch_build_corr_rowmajor(dX.p, (int)n, (int)d, dT.p, p, nugget, dR.p, bad.p, s);
+  ctx->launches += 1;
+  ck(cudaGetLastError(), "build_corr launch");
+  int hbad = 0;
+  ck(cudaMemcpyAsync(R_out, dR.p, n * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H R");
+  ck(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H bad");
+  ck(cudaStreamSynchronize(s), "build_corr");
+  if (hbad) return set_error(GPEMU_NONFINITE, "build_corr_matrix: non-finite correlation value");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size_t n, size_t d,
+                      const double* theta, double p, double* r_out) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !xstar || !X || !theta || !r_out) return set_error(GPEMU_VALIDATION, "corr_vector: null argument");
+  int rc = validate_params(theta, d, p, 0.0);
+  if (rc) return rc;
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  DevBuf<double> dX, dT, dS, dR;
+  DevBuf<int> bad;
+  dX.alloc(n * d);
+  dT.alloc(d);
+  dS.alloc(d);
+  dR.alloc(n);
+  bad.alloc(1);
+  cudaStream_t s = ctx->stream;
+  ck(cudaMemcpyAsync(dX.p, X, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D X");
+  ck(cudaMemcpyAsync(dT.p, theta, d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+  ck(cudaMemcpyAsync(dS.p, xstar, d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D xstar");
+  ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
+  if (n > 0) launch_corr_vectors(dS.p, 1, dX.p, (int)n, (int)d, dT.p, p, dR.p, bad.p, s);
+  ctx->launches += 1;
+  int hbad = 0;
+  ck(cudaMemcpyAsync(r_out, dR.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H r");
+  ck(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H bad");
+  ck(cudaStreamSynchronize(s), "corr_vector");
+  if (hbad) return set_error(GPEMU_NONFINITE, "corr_vector: non-finite correlation value");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+// Factorization workspace for the Backend-level API (one slot, no table).
+int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
+                    double* jitter_used) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !R || n == 0) return set_error(GPEMU_VALIDATION, "factorize: bad argument");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  gpemu_plan pl;
+  pl.ctx = ctx;
+  pl.n = (int)n;
+  pl.NT = (int)((n + TILE - 1) / TILE);
+  pl.Npad = pl.NT * TILE;
+  pl.slot_stride = (size_t)num_tiles(pl.NT) * TILE_ELEMS;
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dR;
+  dR.alloc(n * n);
+  pl.factors.alloc(pl.slot_stride);
+  pl.borders.alloc(2 * pl.Npad);
+  pl.jitter.alloc(1);
+  pl.out.alloc(REC_SIZE);
+  pl.status.alloc(1);
+  pl.slots.alloc(1);
+  pl.flags.alloc((size_t)(pl.NT + 1) * pl.NT);
+  pl.counter.alloc(1);
+  pl.error.alloc(1);
+  ck(cudaMemsetAsync(pl.flags.p, 0, pl.flags.count * sizeof(int), s), "memset");
+  ck(cudaMemsetAsync(pl.slots.p, 0, sizeof(int), s), "memset");
+  ck(cudaMemsetAsync(pl.error.p, 0, sizeof(int), s), "memset");
+  ck(cudaMemcpyAsync(dR.p, R, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D R");
+  for (int step = 0; step < 6; ++step) {
+    const double jit = kLadder[step];
+    ck(cudaMemsetAsync(pl.status.p, 0, sizeof(int), s), "memset");
+    ck(cudaMemsetAsync(pl.borders.p, 0, 2 * pl.Npad * sizeof(double), s), "memset");
+    ck(cudaMemcpyAsync(pl.jitter.p, &jit, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+    launch_rowmajor_to_tiles(dR.p, pl.n, pl.NT, jit, pl.factors.p, s);
+    run_chol(&pl, 1);
+    launch_finalize(pl.factors.p, pl.slot_stride, pl.borders.p, pl.status.p, pl.jitter.p, pl.n,
+                    pl.NT, pl.slots.p, 1, pl.out.p, s);
+    ctx->launches += 2;
+    int st = 0;
+    double rec[REC_SIZE];
+    ck(cudaMemcpyAsync(&st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaMemcpyAsync(rec, pl.out.p, sizeof(rec), cudaMemcpyDeviceToHost, s), "D2H");
+    ck(cudaStreamSynchronize(s), "factorize");
+    int err = 0;
+    ck(cudaMemcpy(&err, pl.error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
+    if (st == 0) {
+      if (L_out) {
+        DevBuf<double> dL;
+        dL.alloc(n * n);
+        launch_tiles_to_rowmajor(pl.factors.p, pl.n, pl.NT, dL.p, s);
+        ctx->launches += 1;
+        ck(cudaMemcpyAsync(L_out, dL.p, n * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
+        ck(cudaStreamSynchronize(s), "factorize");
+      }
+      if (log_det) *log_det = rec[REC_LOGDET];
+      if (jitter_used) *jitter_used = jit;
+      return GPEMU_OK;
+    }
+  }
+  return set_error(GPEMU_NOT_PD, "factorize: not positive definite at any jitter level (n = %zu)", n);
+  GPEMU_GUARD_END
+}
+
+static int solve_common(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x,
+                        int upper) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !L || !b || !x || n == 0) return set_error(GPEMU_VALIDATION, "solve: bad argument");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  const int NT = (int)((n + TILE - 1) / TILE);
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dL, tiles, db, dx;
+  dL.alloc(n * n);
+  tiles.alloc((size_t)num_tiles(NT) * TILE_ELEMS);
+  db.alloc(n);
+  dx.alloc(n);
+  ck(cudaMemcpyAsync(dL.p, L, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D L");
+  ck(cudaMemcpyAsync(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D b");
+  launch_rowmajor_to_tiles(dL.p, (int)n, NT, 0.0, tiles.p, s);
+  launch_tri_solve(tiles.p, (int)n, NT, db.p, dx.p, upper, s);
+  ctx->launches += 2;
+  ck(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H x");
+  ck(cudaStreamSynchronize(s), "solve");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_solve_lower(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x) {
+  return solve_common(ctx, L, n, b, x, 0);
+}
+int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x) {
+  return solve_common(ctx, L, n, b, x, 1);
+}
+
+// ---------------------------------------------------------------------------
+int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
+                      double p, double nugget, size_t max_batch, gpemu_plan** out) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !X || !y || !out) return set_error(GPEMU_VALIDATION, "plan_create: null argument");
+  if (n < 2) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 2 design points");
+  if (d < 1) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 1 input dimension");
+  if (d > 32) return set_error(GPEMU_CONFIG, "plan_create: d = %zu exceeds the device table limit 32", d);
+  if (max_batch < 1) return set_error(GPEMU_VALIDATION, "plan_create: max_batch must be >= 1");
+  int rc = validate_unit_cube(X, n, d, "new_dataset");
+  if (rc) return rc;
+  for (size_t i = 0; i < n; ++i)
+    if (!std::isfinite(y[i])) return set_error(GPEMU_VALIDATION, "new_dataset: non-finite output");
+  std::vector<double> probe(d, 1.0);  // likelihood.hpp:89-90
+  rc = validate_params(probe.data(), d, p, nugget);
+  if (rc) return rc;
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  auto* pl = new gpemu_plan();
+  pl->ctx = ctx;
+  pl->n = (int)n;
+  pl->d = (int)d;
+  pl->p = p;
+  pl->nugget = nugget;
+  pl->NT = (int)((n + TILE - 1) / TILE);
+  pl->Npad = pl->NT * TILE;
+  pl->max_batch = max_batch;
+  pl->nslots = max_batch + 1;
+  pl->slot_stride = (size_t)num_tiles(pl->NT) * TILE_ELEMS;
+  try {
+    pl->X.alloc(n * d);
+    pl->y.alloc(n);
+    pl->table.alloc((size_t)num_tiles(pl->NT) * d * TILE_ELEMS);
+    pl->factors.alloc(pl->nslots * pl->slot_stride);
+    pl->borders.alloc(pl->nslots * 2 * pl->Npad);
+    pl->theta.alloc(pl->nslots * d);
+    pl->jitter.alloc(pl->nslots);
+    pl->out.alloc(pl->nslots * REC_SIZE);
+    pl->status.alloc(pl->nslots);
+    pl->slots.alloc(pl->nslots);
+    pl->flags.alloc(pl->nslots * (size_t)(pl->NT + 1) * pl->NT);
+    pl->counter.alloc(1);
+    pl->error.alloc(1);
+  } catch (const CudaError& e) {
+    delete pl;
+    return set_error(GPEMU_CUDA, "plan_create: device allocation failed (%s)", e.msg.c_str());
+  }
+  cudaStream_t s = ctx->stream;
+  ck(cudaMemcpyAsync(pl->X.p, X, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D X");
+  ck(cudaMemcpyAsync(pl->y.p, y, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D y");
+  ck(cudaMemsetAsync(pl->flags.p, 0, pl->flags.count * sizeof(int), s), "memset flags");
+  ck(cudaMemsetAsync(pl->error.p, 0, sizeof(int), s), "memset error");
+  ck(cudaMemsetAsync(pl->status.p, 0, pl->nslots * sizeof(int), s), "memset status");
+  launch_pow_table(pl->X.p, pl->n, pl->d, p, pl->NT, pl->table.p, s);
+  ctx->launches += 1;
+  ck(cudaGetLastError(), "pow_table launch");
+  ck(cudaStreamSynchronize(s), "plan_create");
+  pl->h_jitter.assign(pl->nslots, 0.0);
+  pl->h_slots.assign(pl->nslots, 0);
+  pl->h_status_all.assign(pl->nslots, 0);
+  pl->h_out.assign(pl->nslots * REC_SIZE, 0.0);
+  *out = pl;
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_plan_destroy(gpemu_plan* plan) {
+  delete plan;
+  return GPEMU_OK;
+}
+
+size_t gpemu_plan_device_bytes(const gpemu_plan* pl) {
+  if (!pl) return 0;
+  return (pl->X.count + pl->y.count + pl->table.count + pl->factors.count + pl->borders.count +
+          pl->theta.count + pl->jitter.count + pl->out.count) *
+             sizeof(double) +
+         (pl->status.count + pl->slots.count + pl->flags.count + 2) * sizeof(int);
+}
+
+int gpemu_eval_batch_device(gpemu_plan* pl, const double* d_theta, size_t B, double* d_out) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !d_theta) return set_error(GPEMU_VALIDATION, "eval_batch_device: null argument");
+  if (B == 0) return GPEMU_OK;
+  if (B > pl->max_batch) return set_error(GPEMU_VALIDATION, "eval_batch: B = %zu exceeds max_batch %zu", B, pl->max_batch);
+  ck(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+  cudaStream_t s = pl->ctx->stream;
+  ck(cudaMemcpyAsync(pl->theta.p, d_theta, B * pl->d * sizeof(double), cudaMemcpyDeviceToDevice, s),
+     "D2D theta");
+  int rc = run_batch(pl, B);
+  if (rc) return rc;
+  if (d_out)
+    ck(cudaMemcpyAsync(d_out, pl->out.p, B * REC_SIZE * sizeof(double), cudaMemcpyDeviceToDevice, s),
+       "D2D out");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_eval_batch(gpemu_plan* pl, const double* theta, size_t B, double* neg2, double* mu,
+                     double* sigma2, double* jitter, double* log_det, int* slot_status) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || (!theta && B)) return set_error(GPEMU_VALIDATION, "eval_batch: null argument");
+  if (B == 0) return GPEMU_OK;
+  if (B > pl->max_batch) return set_error(GPEMU_VALIDATION, "eval_batch: B = %zu exceeds max_batch %zu", B, pl->max_batch);
+  ck(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+  ck(cudaMemcpyAsync(pl->theta.p, theta, B * pl->d * sizeof(double), cudaMemcpyHostToDevice,
+                     pl->ctx->stream),
+     "H2D theta");
+  int rc = run_batch(pl, B);
+  if (rc) return rc;
+  download_records(pl, B);
+  for (size_t b = 0; b < B; ++b) {
+    const double* r = &pl->h_out[b * REC_SIZE];
+    if (neg2) neg2[b] = r[REC_NEG2];
+    if (mu) mu[b] = r[REC_MU];
+    if (sigma2) sigma2[b] = r[REC_SIGMA2];
+    if (jitter) jitter[b] = r[REC_JITTER];
+    if (log_det) log_det[b] = r[REC_LOGDET];
+    if (slot_status) slot_status[b] = (int)r[REC_STATUS];
+  }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_plan_last_factor(gpemu_plan* pl, size_t slot, double* L_out, double* log_det,
+                           double* jitter_used) {
+  GPEMU_GUARD_BEGIN
+  if (!pl) return set_error(GPEMU_VALIDATION, "last_factor: null plan");
+  if (slot >= pl->last_B) return set_error(GPEMU_VALIDATION, "last_factor: slot %zu not in the last batch", slot);
+  if (pl->last_ladder[slot] < 0) return set_error(GPEMU_NOT_PD, "last_factor: slot %zu did not factorize", slot);
+  cudaStream_t s = pl->ctx->stream;
+  if (L_out) {
+    DevBuf<double> dL;
+    dL.alloc((size_t)pl->n * pl->n);
+    launch_tiles_to_rowmajor(pl->factors.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
+    pl->ctx->launches += 1;
+    ck(cudaMemcpyAsync(L_out, dL.p, (size_t)pl->n * pl->n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
+  }
+  double rec[REC_SIZE];
+  ck(cudaMemcpyAsync(rec, pl->out.p + slot * REC_SIZE, sizeof(rec), cudaMemcpyDeviceToHost, s), "D2H rec");
+  ck(cudaStreamSynchronize(s), "last_factor");
+  if (log_det) *log_det = rec[REC_LOGDET];
+  if (jitter_used) *jitter_used = kLadder[pl->last_ladder[slot]];
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+// ---------------------------------------------------------------------------
+int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga_config* gac,
+              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
+              double* trace_best, double* trace_genes, gpemu_model** model_out) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !lo || !hi || !gac) return set_error(GPEMU_VALIDATION, "fit: null argument");
+  const int d = pl->d;
+  const int P = gac->population, G = gac->generations;
+  // GaConfig::validate (optimizer.hpp:29-38)
+  if (P <= 0 || G <= 0) return set_error(GPEMU_VALIDATION, "GaConfig: population and generations must be positive");
+  if (gac->crossover_rate < 0.0 || gac->crossover_rate > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: crossover_rate must be in [0,1]");
+  if (!(gac->mutation_sigma > 0.0)) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_sigma must be positive");
+  if (gac->mutation_prob < 0.0 || gac->mutation_prob > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_prob must be in [0,1]");
+  if (gac->elitism < 0 || gac->elitism >= P) return set_error(GPEMU_VALIDATION, "GaConfig: elitism must be in [0, population)");
+  if ((size_t)P > pl->max_batch) return set_error(GPEMU_CONFIG, "fit: population %d exceeds the plan's max_batch %zu", P, pl->max_batch);
+  // FitConfig::bounds_for (core.hpp:114-123) + log10 box (likelihood.hpp:247-251)
+  std::vector<double> glo(d), ghi(d);
+  for (int k = 0; k < d; ++k) {
+    if (!(lo[k] > 0.0) || !(lo[k] < hi[k])) return set_error(GPEMU_VALIDATION, "FitConfig: theta bounds require 0 < lower < upper");
+    glo[k] = std::log10(lo[k]);
+    ghi[k] = std::log10(hi[k]);
+    if (!(glo[k] < ghi[k]) || !std::isfinite(glo[k]) || !std::isfinite(ghi[k]))
+      return set_error(GPEMU_VALIDATION, "ga_minimize: degenerate bounds");
+  }
+  const uint64_t ga_seed = derive_seed(seed, 0x9a5eedull);
+  const double mut_prob = gac->mutation_prob > 0.0 ? gac->mutation_prob : 1.0 / (double)d;
+  const int stash = (int)pl->max_batch;  // device slot holding the best factor
+  cudaStream_t s = pl->ctx->stream;
+
+  // lhs_population (optimizer.hpp:62-80)
+  Rng init_rng(derive_seed(ga_seed, 0x1e17u));
+  std::vector<std::vector<double>> pop(P, std::vector<double>(d));
+  {
+    std::vector<int> perm(P);
+    for (int k = 0; k < d; ++k) {
+      std::iota(perm.begin(), perm.end(), 0);
+      for (int i = P - 1; i > 0; --i) {
+        const int j = (int)init_rng.below((uint64_t)i + 1);
+        std::swap(perm[i], perm[j]);
+      }
+      const double width = ghi[k] - glo[k];
+      for (int i = 0; i < P; ++i) {
+        const double u = (perm[i] + init_rng.uniform01()) / P;
+        pop[i][k] = glo[k] + width * u;
+      }
+    }
+  }
+  std::vector<double> fitness(P), thetas((size_t)P * d);
+  double best_value = INFINITY, stash_value = INFINITY, jitter_max = 0.0;
+  std::vector<double> best_point, stash_theta(d), stash_rec(REC_SIZE, 0.0);
+  std::vector<double> tb(G), tg((size_t)G * d);
+
+  for (int gen = 0; gen < G; ++gen) {
+    if (gen > 0) {
+      std::vector<std::vector<double>> next(P);
+      std::vector<int> order(P);
+      std::iota(order.begin(), order.end(), 0);
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return fitness[a] < fitness[b]; });
+      for (int e = 0; e < gac->elitism; ++e) next[e] = pop[order[e]];
+      for (int slot = gac->elitism; slot < P; ++slot) {
+        Rng rng(derive_seed(ga_seed, (uint64_t)gen, (uint64_t)slot));
+        auto tournament = [&]() -> const std::vector<double>& {
+          const int a = (int)rng.below(P);
+          const int b = (int)rng.below(P);
+          const bool a_wins = fitness[a] < fitness[b] || (fitness[a] == fitness[b] && a <= b);
+          return pop[a_wins ? a : b];
+        };
+        const auto& pa = tournament();
+        const auto& pb = tournament();
+        std::vector<double> child(d);
+        if (rng.uniform01() < gac->crossover_rate) {
+          for (int k = 0; k < d; ++k) child[k] = rng.uniform01() < 0.5 ? pa[k] : pb[k];
+        } else {
+          child = pa;
+        }
+        for (int k = 0; k < d; ++k) {
+          if (rng.uniform01() < mut_prob) child[k] += gac->mutation_sigma * rng.normal();
+          child[k] = std::clamp(child[k], glo[k], ghi[k]);
+        }
+        next[slot] = std::move(child);
+      }
+      pop = std::move(next);
+    }
+    // objective lambda (likelihood.hpp:264-273) over the whole generation
+    for (int i = 0; i < P; ++i)
+      for (int k = 0; k < d; ++k) thetas[(size_t)i * d + k] = std::pow(10.0, pop[i][k]);
+    ck(cudaMemcpyAsync(pl->theta.p, thetas.data(), thetas.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, s),
+       "H2D theta");
+    int rc = run_batch(pl, P);
+    if (rc) return rc;
+    download_records(pl, P);
+    for (int i = 0; i < P; ++i) {
+      const double* r = &pl->h_out[(size_t)i * REC_SIZE];
+      fitness[i] = r[REC_NEG2];
+      if (pl->last_ladder[i] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[i]]);
+      if (fitness[i] < stash_value) {  // strict <, call order = (generation, slot)
+        stash_value = fitness[i];
+        std::copy(r, r + REC_SIZE, stash_rec.begin());
+        std::copy(&thetas[(size_t)i * d], &thetas[(size_t)i * d] + d, stash_theta.begin());
+        ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
+                           pl->factors.p + (size_t)i * pl->slot_stride,
+                           pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
+           "stash factor");
+        ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
+                           pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s),
+           "stash border");
+      }
+    }
+    // record_generation (optimizer.hpp:133-141)
+    int b = 0;
+    for (int i = 1; i < P; ++i)
+      if (fitness[i] < fitness[b]) b = i;
+    if (fitness[b] < best_value) {
+      best_value = fitness[b];
+      best_point = pop[b];
+    }
+    tb[gen] = fitness[b];
+    std::copy(pop[b].begin(), pop[b].end(), tg.begin() + (size_t)gen * d);
+  }
+  ck(cudaStreamSynchronize(s), "fit");
+  if (!std::isfinite(stash_value))
+    return set_error(GPEMU_FIT, "fit_gp: every candidate failed factorization (n = %d)", pl->n);
+  if (best_value != stash_value)
+    return set_error(GPEMU_ERROR, "fit_gp: optimizer incumbent diverged from evaluation stash");
+  gpemu_model* m = make_model(pl, stash, stash_theta.data(), stash_rec.data());
+  if (theta_hat) std::copy(stash_theta.begin(), stash_theta.end(), theta_hat);
+  if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+  if (trace_best) std::copy(tb.begin(), tb.end(), trace_best);
+  if (trace_genes) std::copy(tg.begin(), tg.end(), trace_genes);
+  if (res) {
+    res->neg2_log_lik = stash_rec[REC_NEG2];
+    res->mu_hat = stash_rec[REC_MU];
+    res->sigma2_hat = stash_rec[REC_SIGMA2];
+    res->jitter_max = jitter_max;
+    res->r_builds = pl->r_builds;
+    res->factorizations = pl->factorizations;
+    res->triangular_solves = pl->solves;
+  }
+  if (model_out) {
+    *model_out = m;
+  } else {
+    delete m;
+  }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_model_at_theta(gpemu_plan* pl, const double* theta, gpemu_model** model_out,
+                         double* scalars, double* alpha) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !theta) return set_error(GPEMU_VALIDATION, "model_at_theta: null argument");
+  cudaStream_t s = pl->ctx->stream;
+  ck(cudaMemcpyAsync(pl->theta.p, theta, pl->d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+  int rc = run_batch(pl, 1);
+  if (rc) return rc;
+  download_records(pl, 1);
+  const double* r = pl->h_out.data();
+  if (!std::isfinite(r[REC_NEG2]))
+    return set_error(GPEMU_NOT_PD, "model_at_theta: factorization failed at the requested theta");
+  gpemu_model* m = make_model(pl, 0, theta, r);
+  if (scalars) {
+    scalars[0] = m->neg2;
+    scalars[1] = m->mu;
+    scalars[2] = m->sigma2;
+    scalars[3] = m->jitter;
+  }
+  if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+  if (model_out) {
+    *model_out = m;
+  } else {
+    delete m;
+  }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_model_destroy(gpemu_model* m) {
+  delete m;
+  return GPEMU_OK;
+}
+
+int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, double* mse) {
+  GPEMU_GUARD_BEGIN
+  if (!m || (!Xtest && N) || (!yhat && N)) return set_error(GPEMU_VALIDATION, "predict: null argument");
+  int rc = validate_unit_cube(Xtest, N, m->d, "predict");
+  if (rc) return set_error(GPEMU_VALIDATION, "predict: test point outside the unit cube");
+  if (N == 0) return GPEMU_OK;
+  ck(cudaSetDevice(m->ctx->device), "cudaSetDevice");
+  cudaStream_t s = m->ctx->stream;
+  DevBuf<double> dXt, dy, dm;
+  DevBuf<int> bad;
+  dXt.alloc(N * m->d);
+  dy.alloc(N);
+  bad.alloc(1);
+  ck(cudaMemcpyAsync(dXt.p, Xtest, N * m->d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D Xtest");
+  ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
+  launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p, dy.p,
+                 bad.p, s);
+  m->ctx->launches += 1;
+  if (mse) {
+    dm.alloc(N);
+    launch_predict_mse(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->sigma2,
+                       m->tiles.p, m->NT, m->v.p, m->vtv, nullptr, dm.p, bad.p, s);
+    m->ctx->launches += 1;
+  }
+  ck(cudaGetLastError(), "predict launch");
+  int hbad = 0;
+  ck(cudaMemcpyAsync(yhat, dy.p, N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H yhat");
+  if (mse) ck(cudaMemcpyAsync(mse, dm.p, N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H mse");
+  ck(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H bad");
+  ck(cudaStreamSynchronize(s), "predict");
+  if (hbad) return set_error(GPEMU_NONFINITE, "corr_vector: non-finite correlation value");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+}  // extern "C"

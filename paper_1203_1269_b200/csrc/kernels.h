@@ -1,0 +1,75 @@
+// kernels.h -- host-side launchers for the sm_100a kernels (no torch types).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace gpemu_dev {
+
+// ---- K1: correlation (kernels_corr.cu) -------------------------------------
+// CorrelationPlan ctor (correlation.hpp:156-180): |x_ik - x_jk|^p for every
+// lower-tile element, tile-major [tile][k][elem].
+void launch_pow_table(const double* X, int n, int d, double p, int NT, double* table,
+                      cudaStream_t s);
+// CorrelationPlan::build_into (:187-223) + the ladder's diagonal jitter
+// (backend.hpp:106-109) + border rows [y; 1] for every listed slot.
+// slots[q] (q < nslots) indexes the slot; jitter[slot] is added to the diagonal.
+void launch_assemble(const double* table, const double* theta /*[slot][d]*/, const double* y,
+                     int n, int d, double nugget, int NT, const int* slots, int nslots,
+                     const double* jitter, double* factors, size_t slot_stride, double* borders,
+                     int* status, cudaStream_t s);
+// Row-major n x n R for one theta (build_corr_matrix, correlation.hpp:99-146).
+void launch_build_corr_rowmajor(const double* X, int n, int d, const double* theta, double p,
+                                double nugget, double* R, int* bad, cudaStream_t s);
+// Cross-correlation matrix r[j][i] for test points (corr_vector, :67-91).
+void launch_corr_vectors(const double* Xt, int N, const double* X, int n, int d,
+                         const double* theta, double p, double* r, int* bad, cudaStream_t s);
+
+// ---- K2: Cholesky (kernels_chol.cu) ----------------------------------------
+struct DagLaunch {
+  double* factors;
+  double* borders;
+  size_t slot_stride;
+  int n, NT;
+  const int* slots;
+  int nslots;
+  int* counter;
+  int* flags;      // [slot][NT+1][NT]
+  int epoch;
+  int* status;     // [slot]
+  int* error;      // deadlock / timeout word
+};
+void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s);
+void launch_chol_simple(const DagLaunch& a, cudaStream_t s);
+size_t chol_dag_smem_bytes();
+
+// ---- K3: deviance (kernels_misc.cu) ----------------------------------------
+// ProfileEvaluator::eval tail (likelihood.hpp:124-140).
+void launch_finalize(const double* factors, size_t slot_stride, const double* borders,
+                     const int* status, const double* jitter, int n, int NT, const int* slots,
+                     int nslots, double* out /*[slot][REC_SIZE]*/, cudaStream_t s);
+
+// ---- layout conversions / solves (kernels_misc.cu) -------------------------
+// Row-major n x n (lower used) + jitter on diagonal -> tiled slot storage.
+void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, double* tiles,
+                              cudaStream_t s);
+// Tiled -> row-major lower with strict upper zeroed.
+void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s);
+// Forward (upper=0: L x = b) or backward (upper=1: L^T x = b) substitution on a
+// tiled factor (backend.hpp:129-153). One CTA.
+void launch_tri_solve(const double* tiles, int n, int NT, const double* b, double* x, int upper,
+                      cudaStream_t s);
+
+// ---- K4: prediction (kernels_predict.cu) -----------------------------------
+// yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50); when mse is
+// non-null also w = L^-1 r_j and the kriging MSE.
+void launch_predict(const double* Xt, int N, const double* X, int n, int d, const double* theta,
+                    double p, double mu, const double* alpha, double* yhat, int* bad,
+                    cudaStream_t s);
+void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
+                        const double* theta, double p, double sigma2, const double* tiles, int NT,
+                        const double* v /* L^-1 1 */, double vtv, double* work /*N*Npad*/,
+                        double* mse, int* bad, cudaStream_t s);
+
+}  // namespace gpemu_dev

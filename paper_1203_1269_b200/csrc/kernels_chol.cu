@@ -1,0 +1,521 @@
+// kernels_chol.cu -- K2: batched FP64 Cholesky of R + jitter*I on sm_100a.
+//
+// Reference: backend.hpp (relative to /root/reference/proj/include/gpemu/)
+//   factorize_into     :102-120  jitter ladder, pivot test !(s > 0), log-det
+//   ReferenceBackend   :189-206  unblocked dot-product Cholesky
+//   ParallelBackend    :226-311  right-looking 64-blocked Cholesky
+//   solve_lower_into   :129-140  u = L^-1 y, v = L^-1 1 (likelihood.hpp:122-123)
+//
+// Two engines over the same tiled HBM layout (layout.cuh):
+//
+// * chol_dag_kernel -- the product engine. A persistent kernel (one CTA per SM)
+//   pulls tasks from a global ticket counter. The task order is a topological
+//   order of the left-looking tile Cholesky of every candidate in the batch,
+//   with a one-column lookahead (the diagonal task of column j+1 is issued right
+//   after the task that produces its last input), so waits only ever target
+//   lower tickets (deadlock free) and the serial panel chain of one candidate
+//   is hidden behind the other candidates' work.
+//     DIAG(b, j):  C = R(j,j) - sum_{K<j} L(j,K) L(j,K)^T     (DMMA)
+//                  L(j,j) = chol(C)      blocked 16-wide in shared memory
+//                  border rows: [u_j; v_j] = ([y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T) L(j,j)^-T
+//     OFF(b, j, I): C = R(I,j) - sum_{K<j} L(I,K) L(j,K)^T    (DMMA)
+//                  L(I,j) = C L(j,j)^-T  blocked 16-wide (substitution + DMMA updates)
+//   The two forward solves of the reference are the bordered rows [y 1]^T of
+//   the factorization, so u and v fall out of the same tile pass and the solves
+//   never re-read L. Operand k-slabs (128 x 32 doubles, 32 KB) are streamed by a
+//   producer warp with cp.async.bulk (TMA) into a 3-stage mbarrier ring; eight
+//   consumer warps run m8n8k4 DMMA on a 128x128 accumulator tile (64x32 per warp).
+//
+// * chol_simple_kernel -- validation engine: one CTA per candidate, unblocked
+//   right-looking, products and differences rounded separately, so on identical
+//   R it reproduces the reference's arithmetic order bit for bit.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "kernels.h"
+#include "layout.cuh"
+#include "ptx.cuh"
+
+namespace gpemu_dev {
+
+// ============================================================================
+// Simple engine
+// ============================================================================
+
+__device__ __forceinline__ double* tile_elem(double* base, int i, int j) {
+  return base + tile_index(i >> 7, j >> 7) * TILE_ELEMS + elem_off(i & 127, j & 127);
+}
+
+__global__ void __launch_bounds__(1024) chol_simple_kernel(DagLaunch a) {
+  const int slot = a.slots[blockIdx.x];
+  double* base = a.factors + (size_t)slot * a.slot_stride;
+  const int Npad = a.NT * TILE;
+  double* u = a.borders + (size_t)slot * 2 * Npad;
+  double* v = u + Npad;
+  __shared__ double dsh;
+  __shared__ int fail;
+  if (threadIdx.x == 0) fail = (a.status[slot] != 0);
+  __syncthreads();
+  if (fail) return;
+  for (int k = 0; k < Npad; ++k) {
+    if (threadIdx.x == 0) {
+      const double s = *tile_elem(base, k, k);
+      if (!(s > 0.0)) {
+        fail = 1;
+      } else {
+        const double dd = sqrt(s);
+        *tile_elem(base, k, k) = dd;
+        dsh = dd;
+      }
+    }
+    __syncthreads();
+    if (fail) break;
+    const double dd = dsh;
+    for (int i = k + 1 + threadIdx.x; i < Npad; i += blockDim.x) {
+      double* p = tile_elem(base, i, k);
+      *p = *p / dd;
+    }
+    if (threadIdx.x == 0) {
+      u[k] = u[k] / dd;
+      v[k] = v[k] / dd;
+    }
+    __syncthreads();
+    const int m = Npad - k - 1;
+    const long long npairs = (long long)m * (m + 1) / 2;
+    for (long long q = threadIdx.x; q < npairs; q += blockDim.x) {
+      int ii = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
+      while ((long long)(ii + 1) * (ii + 2) / 2 <= q) ++ii;
+      while ((long long)ii * (ii + 1) / 2 > q) --ii;
+      const int ll = (int)(q - (long long)ii * (ii + 1) / 2);
+      const int i = k + 1 + ii, l = k + 1 + ll;
+      double* p = tile_elem(base, i, l);
+      *p = __dsub_rn(*p, __dmul_rn(*tile_elem(base, i, k), *tile_elem(base, l, k)));
+    }
+    for (int l = k + 1 + threadIdx.x; l < Npad; l += blockDim.x) {
+      const double lk = *tile_elem(base, l, k);
+      u[l] = __dsub_rn(u[l], __dmul_rn(u[k], lk));
+      v[l] = __dsub_rn(v[l], __dmul_rn(v[k], lk));
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && fail) a.status[slot] = 1;  // GPEMU_SLOT_NOT_PD
+}
+
+void launch_chol_simple(const DagLaunch& a, cudaStream_t s) {
+  chol_simple_kernel<<<a.nslots, 1024, 0, s>>>(a);
+}
+
+// ============================================================================
+// DAG engine
+// ============================================================================
+
+namespace {
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = kConsumerWarps * 32;  // 256
+constexpr int kThreads = kConsumers + 32;        // + producer warp
+constexpr int kStages = 3;
+constexpr int kSlabBytes = SLAB_ELEMS * 8;              // 32 KB
+constexpr int kStageBytes = 2 * kSlabBytes;             // A + B slab
+constexpr int kOffStages = 0;                           // [0, 192K)
+constexpr int kOffC = 0;                                // epilogue tile [0, 128K)
+constexpr int kOffStrip = 128 * 1024;                   // 2 x 32 KB [128K, 192K)
+constexpr int kOffBar = kStages * kStageBytes;          // 192K: mbarriers
+constexpr int kOffW = kOffBar + 256;                    // border w: 2 x 128 doubles
+constexpr int kOffMisc = kOffW + 2 * TILE * 8;          // task scalars
+constexpr int kSmemBytes = kOffMisc + 64;
+constexpr long long kSpinLimitCycles = 20000000000LL;  // ~10 s: declare deadlock
+
+struct Misc {
+  int ticket;
+  int skip;
+  int fail;
+  int pad;
+};
+
+__device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
+
+// Spin until *flag == epoch (acquire). On timeout record an error and proceed.
+__device__ __forceinline__ void wait_flag(const int* flag, int epoch, int* error) {
+  if (ld_acquire_gpu(flag) == epoch) return;
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(flag) != epoch) {
+    __nanosleep(64);
+    if (clock64() - t0 > kSpinLimitCycles) {
+      atomicExch(error, 1);
+      return;
+    }
+  }
+}
+
+__device__ __forceinline__ void publish_flag(int* flag, int epoch) {
+  __threadfence();
+  fence_proxy_async_global();
+  st_release_gpu(flag, epoch);
+}
+
+// Task decode (see header comment): ticket -> (bpos, j, I).
+__device__ __forceinline__ void decode_task(int t, int B, int NT, int& bpos, int& j, int& I) {
+  if (t < B) {
+    bpos = t;
+    j = 0;
+    I = 0;
+    return;
+  }
+  t -= B;
+  int jj = 0;
+  while (true) {
+    const int g = B * (NT - jj);
+    if (t < g) break;
+    t -= g;
+    ++jj;
+  }
+  const int per = NT - jj;
+  bpos = t / per;
+  const int pos = t - bpos * per;
+  if (pos == 0) {
+    j = jj;
+    I = jj + 1;
+  } else if (pos == 1) {
+    j = jj + 1;
+    I = jj + 1;
+  } else {
+    j = jj;
+    I = jj + pos;
+  }
+}
+
+// C tile accessors in shared memory (tile layout).
+__device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_off(r, c)]; }
+
+// Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16).
+// Returns false (uniform across the warp) on a failed pivot.
+__device__ bool potrf16(double* C, int o, int lane) {
+  for (int c = 0; c < 16; ++c) {
+    double dval = 0.0;
+    int ok = 1;
+    if (lane == c) {
+      double s = Cs(C, o + c, o + c);
+      for (int t = 0; t < c; ++t) {
+        const double l = Cs(C, o + c, o + t);
+        s -= l * l;
+      }
+      ok = s > 0.0;  // backend.hpp:238 pivot test, NaN-safe
+      dval = ok ? sqrt(s) : 0.0;
+      if (ok) Cs(C, o + c, o + c) = dval;
+    }
+    dval = __shfl_sync(0xffffffffu, dval, c);
+    ok = __shfl_sync(0xffffffffu, ok, c);
+    if (!ok) return false;
+    if (lane > c && lane < 16) {
+      double x = Cs(C, o + lane, o + c);
+      for (int t = 0; t < c; ++t) x -= Cs(C, o + lane, o + t) * Cs(C, o + c, o + t);
+      Cs(C, o + lane, o + c) = x / dval;
+    }
+    __syncwarp();
+  }
+  return true;
+}
+
+// C[rows >= r0 of warp, cols n >= n0] -= A_rows * B^T with K = 16 columns at
+// offset ko; B rows read through bfetch(row, k). Warp w owns rows [16w, 16w+16).
+template <typename BFetch>
+__device__ __forceinline__ void warp_update16(double* C, int warp, int lane, int ko, int nb_lo,
+                                              int nb_hi, BFetch bfetch) {
+  const int lr = lane >> 2, lc = lane & 3;
+  double a[2][4];
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) a[mi][ks] = -Cs(C, 16 * warp + 8 * mi + lr, ko + 4 * ks + lc);
+  for (int nb = nb_lo; nb <= nb_hi; ++nb) {
+    double b[4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) b[ks] = bfetch(8 * nb + lr, ko + 4 * ks + lc);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int r = 16 * warp + 8 * mi + lr;
+      double2* p = reinterpret_cast<double2*>(&Cs(C, r, 8 * nb + 2 * lc));
+      double2 acc = *p;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) dmma884(acc.x, acc.y, a[mi][ks], b[ks]);
+      *p = acc;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* empty = full + kStages;
+  double* C = reinterpret_cast<double*>(smem + kOffC);
+  double* strip = reinterpret_cast<double*>(smem + kOffStrip);
+  double* W = reinterpret_cast<double*>(smem + kOffW);
+  Misc* misc = reinterpret_cast<Misc*>(smem + kOffMisc);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int NT = a.NT, B = a.nslots, n = a.n;
+  const int Npad = NT * TILE;
+  const int ntasks = B * NT * (NT + 1) / 2;
+  const int epoch = a.epoch;
+  const size_t fstride = (size_t)(NT + 1) * NT;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  uint32_t it = 0;  // slab iteration counter, advanced identically by both roles
+  while (true) {
+    if (tid == kConsumers) {
+      const int t = atomicAdd(a.counter, 1);
+      misc->ticket = t;
+      if (t < ntasks) {
+        int bpos, j, I;
+        decode_task(t, B, NT, bpos, j, I);
+        misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
+      }
+      misc->fail = 0;
+    }
+    __syncthreads();
+    const int t = misc->ticket;
+    if (t >= ntasks) break;
+    int bpos, j, I;
+    decode_task(t, B, NT, bpos, j, I);
+    const bool diag = (I == j);
+    const int slot = a.slots[bpos];
+    const bool skip = misc->skip != 0;
+    double* fac = a.factors + (size_t)slot * a.slot_stride;
+    double* bord = a.borders + (size_t)slot * 2 * Npad;
+    int* flags = a.flags + (size_t)slot * fstride;  // flags[I*NT + J], border row I = NT
+    const int nslab = skip ? 0 : SLABS_PER_TILE * j;
+
+    if (warp == kConsumerWarps) {
+      // ------------------------------ producer ------------------------------
+      if (lane == 0) {
+        for (int q = 0; q < nslab; ++q, ++it) {
+          const int K = q >> 2, sq = q & 3;
+          if (sq == 0) {
+            wait_flag(&flags[j * NT + K], epoch, a.error);
+            if (diag) {
+              wait_flag(&flags[NT * NT + K], epoch, a.error);
+            } else {
+              wait_flag(&flags[I * NT + K], epoch, a.error);
+            }
+            fence_proxy_async_global();
+          }
+          const int stage = it % kStages;
+          const uint32_t round = it / kStages;
+          if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
+          unsigned char* dst = smem + kOffStages + stage * kStageBytes;
+          mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
+          bulk_g2s(dst, fac + tile_index(I, K) * TILE_ELEMS + sq * SLAB_ELEMS, kSlabBytes,
+                   &full[stage]);
+          if (!diag) {
+            bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
+                     kSlabBytes, &full[stage]);
+          }
+        }
+      } else {
+        it += nslab;
+      }
+    } else {
+      // ------------------------------ consumers -----------------------------
+      const int wm = warp >> 2, wn = warp & 3;
+      const int lr = lane >> 2, lc = lane & 3;
+      const int brow = tid >> 7, bc = tid & 127;  // border accumulation role (DIAG)
+      double acc[8][4][2];
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      double wacc = 0.0;
+
+      for (int q = 0; q < nslab; ++q, ++it) {
+        const int stage = it % kStages;
+        const uint32_t round = it / kStages;
+        mbar_wait(&full[stage], round & 1);
+        const double* As = reinterpret_cast<const double*>(smem + kOffStages + stage * kStageBytes);
+        const double* Bs = diag ? As : As + SLAB_ELEMS;
+        const double* Aw = As + (wm * 64 + lr) * 32 + lc;
+        const double* Bw = Bs + (wn * 32 + lr) * 32 + lc;
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const int ko = (ks ^ lr) << 2;
+          double av[8], bv[4];
+#pragma unroll
+          for (int mi = 0; mi < 8; ++mi) av[mi] = Aw[mi * 256 + ko];
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) bv[ni] = Bw[ni * 256 + ko];
+#pragma unroll
+          for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+        }
+        if (diag) {
+          // border rows: wacc += sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk]
+          const int K = q >> 2, sq = q & 3;
+          const double* ub = bord + brow * Npad + K * TILE + sq * SLAB;
+#pragma unroll 8
+          for (int kk = 0; kk < SLAB; ++kk) wacc += __ldcg(ub + kk) * Bs[slab_off(bc, kk)];
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      consumer_sync();  // every consumer is done reading the stage ring
+
+      // accumulators -> C (tile layout); C = R - acc
+#pragma unroll
+      for (int mi = 0; mi < 8; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < 4; ++ni) {
+          const int r = wm * 64 + mi * 8 + lr;
+          const int off = wn * 4096 + r * 32 + ((((2 * ni + (lc >> 1)) ^ lr)) << 2) + 2 * (lc & 1);
+          *reinterpret_cast<double2*>(C + off) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        }
+      consumer_sync();
+      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
+      if (!skip) {
+        for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers) {
+          const double2 r = __ldcg(reinterpret_cast<const double2*>(gtile + e));
+          double2* cp = reinterpret_cast<double2*>(C + e);
+          const double2 s = *cp;
+          *cp = make_double2(r.x - s.x, r.y - s.y);
+        }
+      }
+      consumer_sync();
+
+      if (diag) {
+        // ------------------------------ DIAG ------------------------------
+        bool ok = !skip;
+        if (!skip) {
+          W[brow * TILE + bc] = __ldcg(bord + brow * Npad + j * TILE + bc) - wacc;
+          for (int kb = 0; kb < 8 && ok; ++kb) {
+            const int o = 16 * kb;
+            if (warp == 0) {
+              if (!potrf16(C, o, lane) && lane == 0) misc->fail = 1;
+            }
+            consumer_sync();
+            if (misc->fail) {
+              ok = false;
+              break;
+            }
+            // panel rows below the 16x16 block
+            const int r = o + 16 + tid;
+            if (r < TILE) {
+              double x[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) x[c] = Cs(C, r, o + c);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+#pragma unroll
+                for (int tt = 0; tt < c; ++tt) x[c] -= x[tt] * Cs(C, o + c, o + tt);
+                x[c] = x[c] / Cs(C, o + c, o + c);
+              }
+#pragma unroll
+              for (int c = 0; c < 16; ++c) Cs(C, r, o + c) = x[c];
+            }
+            consumer_sync();
+            // trailing lower update with the 16-wide panel (DMMA)
+            if (16 * warp >= o + 16) {
+              warp_update16(C, warp, lane, o, (o + 16) >> 3, 2 * warp + 1,
+                            [&](int row, int k) { return Cs(C, row, k); });
+            }
+            consumer_sync();
+          }
+          if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
+        }
+        // L(j,j) -> HBM, then publish
+        if (ok) {
+          for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
+            __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
+        }
+        consumer_sync();
+        if (tid == 0) publish_flag(&flags[j * NT + j], epoch);
+        // border solve: [u_j; v_j] = w L(j,j)^-T (column-oriented substitution)
+        if (ok && warp < 2) {
+          double* w = W + warp * TILE;
+          for (int c = 0; c < TILE; ++c) {
+            const double x = w[c] / Cs(C, c, c);
+            __syncwarp();
+            for (int l = c + 1 + lane; l < TILE; l += 32) w[l] -= x * Cs(C, l, c);
+            if (lane == 0) w[c] = x;
+            __syncwarp();
+          }
+          for (int l = lane; l < TILE; l += 32) __stcg(bord + warp * Npad + j * TILE + l, w[l]);
+        }
+        consumer_sync();
+        if (tid == 0) publish_flag(&flags[NT * NT + j], epoch);
+      } else {
+        // ------------------------------ OFF -------------------------------
+        if (tid == 0) wait_flag(&flags[j * NT + j], epoch, a.error);
+        consumer_sync();
+        const bool run = !skip && *((volatile int*)&a.status[slot]) == 0;
+        if (run) {
+          const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
+          for (int cb = 0; cb < 8; ++cb) {
+            const int s = cb >> 1;
+            double* buf = strip + (s & 1) * SLAB_ELEMS;
+            if ((cb & 1) == 0) {
+              for (int e = 2 * tid; e < SLAB_ELEMS; e += 2 * kConsumers)
+                *reinterpret_cast<double2*>(buf + e) =
+                    __ldcg(reinterpret_cast<const double2*>(Ljj + s * SLAB_ELEMS + e));
+              consumer_sync();
+            }
+            const int o = 16 * cb;
+            const int ko = o - 32 * s;  // column offset inside the slab
+            // (a) 16-column substitution, one row per thread
+            if (tid < TILE) {
+              const int r = tid;
+              double x[16];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) x[c] = Cs(C, r, o + c);
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+#pragma unroll
+                for (int tt = 0; tt < c; ++tt) x[c] -= x[tt] * buf[slab_off(o + c, ko + tt)];
+                x[c] = x[c] / buf[slab_off(o + c, ko + c)];
+              }
+#pragma unroll
+              for (int c = 0; c < 16; ++c) Cs(C, r, o + c) = x[c];
+            }
+            consumer_sync();
+            // (b) C[:, >= o+16] -= X[:, o:o+16] * L(j,j)[>= o+16, o:o+16]^T
+            if (cb < 7) {
+              warp_update16(C, warp, lane, o, (o + 16) >> 3, 15,
+                            [&](int row, int k) { return buf[slab_off(row, k - 32 * s)]; });
+            }
+            consumer_sync();
+          }
+          for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
+            __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
+        }
+        consumer_sync();
+        if (tid == 0) publish_flag(&flags[I * NT + j], epoch);
+      }
+    }
+    __syncthreads();
+  }
+}
+}  // namespace
+
+size_t chol_dag_smem_bytes() { return kSmemBytes; }
+
+void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    configured = true;
+  }
+  const int ntasks = a.nslots * a.NT * (a.NT + 1) / 2;
+  const int grid = ntasks < num_sms ? ntasks : num_sms;
+  cudaMemsetAsync(a.counter, 0, sizeof(int), s);
+  chol_dag_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
+}
+
+}  // namespace gpemu_dev

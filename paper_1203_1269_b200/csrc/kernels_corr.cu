@@ -1,0 +1,192 @@
+// kernels_corr.cu -- K1: power-exponential correlation assembly on sm_100a.
+//
+// Reference: correlation.hpp (paths relative to /root/reference/proj/include/gpemu/).
+//   pow_abs            :31-35   |dx|^p = exp(p log|dx|), dx == 0 -> 0
+//   theta_weighted_sum :42-47   sum_k theta_k * term_k, sequential in k,
+//                               products and sums rounded separately
+//   CorrelationPlan    :156-180 per-design |dx|^p table
+//   build_into         :187-223 R_ij = exp(-s), R_ii = 1 + nugget
+// The sequential, separately rounded sum is reproduced with __dmul_rn /
+// __dadd_rn (no FMA contraction); exp/log are CUDA libdevice (<= 1 ulp from
+// glibc), so R agrees with the reference to ~1e-16 relative, not bitwise.
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "layout.cuh"
+
+namespace gpemu_dev {
+
+constexpr int kMaxD = 32;  // input dimensions supported by the register-resident table path
+
+__device__ __forceinline__ double pow_abs(double delta, double p) {
+  if (delta == 0.0) return 0.0;
+  const double a = delta < 0.0 ? -delta : delta;
+  return exp(__dmul_rn(p, log(a)));
+}
+
+// Table: [tile][k][elem], tile-major over the packed lower tiles.
+__global__ void pow_table_kernel(const double* __restrict__ X, int n, int d, double p, int NT,
+                                 double* __restrict__ table) {
+  const int tile = blockIdx.x;
+  // tile -> (I, J)
+  int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  while (I * (I + 1) / 2 > tile) --I;
+  const int J = tile - I * (I + 1) / 2;
+  double* out = table + (size_t)tile * d * TILE_ELEMS;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    int r, c;
+    elem_rc(e, r, c);
+    const int i = I * TILE + r, j = J * TILE + c;
+    const bool live = i < n && j < n && i != j;
+    for (int k = 0; k < d; ++k) {
+      double v = 0.0;
+      if (live) v = pow_abs(X[(size_t)i * d + k] - X[(size_t)j * d + k], p);
+      out[(size_t)k * TILE_ELEMS + e] = v;
+    }
+  }
+}
+
+void launch_pow_table(const double* X, int n, int d, double p, int NT, double* table,
+                      cudaStream_t s) {
+  dim3 grid(num_tiles(NT), 16);
+  pow_table_kernel<<<grid, 256, 0, s>>>(X, n, d, p, NT, table);
+}
+
+// Border rows [y; 1] (the bordered-matrix form of the two forward solves,
+// likelihood.hpp:122-123) and the slot status reset.
+__global__ void border_init_kernel(const double* __restrict__ y, int n, int Npad,
+                                   const int* __restrict__ slots, double* __restrict__ borders,
+                                   int* __restrict__ status) {
+  const int slot = slots[blockIdx.y];
+  double* u = borders + (size_t)slot * 2 * Npad;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < Npad; i += gridDim.x * blockDim.x) {
+    u[i] = i < n ? y[i] : 0.0;
+    u[Npad + i] = i < n ? 1.0 : 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) status[slot] = 0;
+}
+
+constexpr int kAsmSlotChunk = 64;
+
+__global__ void __launch_bounds__(256) assemble_kernel(
+    const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
+    double nugget, int NT, const int* __restrict__ slots, int nslots,
+    const double* __restrict__ jitter, double* __restrict__ factors, size_t slot_stride,
+    int* __restrict__ status) {
+  __shared__ double th[kAsmSlotChunk * kMaxD];
+  __shared__ int sl[kAsmSlotChunk];
+  const int tile = blockIdx.x;
+  int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  while (I * (I + 1) / 2 > tile) --I;
+  const int J = tile - I * (I + 1) / 2;
+  const double* tb = table + (size_t)tile * d * TILE_ELEMS;
+  const double diag_base = __dadd_rn(1.0, nugget);  // correlation.hpp:193
+
+  for (int c0 = 0; c0 < nslots; c0 += kAsmSlotChunk) {
+    const int cn = min(kAsmSlotChunk, nslots - c0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < cn * d; q += blockDim.x) {
+      const int si = q / d, k = q - si * d;
+      th[si * kMaxD + k] = theta[(size_t)slots[c0 + si] * d + k];
+    }
+    for (int q = threadIdx.x; q < cn; q += blockDim.x) sl[q] = slots[c0 + q];
+    __syncthreads();
+    for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS;
+         e += gridDim.y * blockDim.x) {
+      int r, c;
+      elem_rc(e, r, c);
+      const int i = I * TILE + r, j = J * TILE + c;
+      double t[kMaxD];
+#pragma unroll
+      for (int k = 0; k < kMaxD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
+      const bool pad = i >= n || j >= n;
+      for (int si = 0; si < cn; ++si) {
+        const int slot = sl[si];
+        double v;
+        if (pad) {
+          v = (i == j) ? 1.0 : 0.0;
+        } else if (i == j) {
+          v = __dadd_rn(diag_base, jitter[slot]);  // backend.hpp:107-109
+        } else {
+          double s = 0.0;
+#pragma unroll
+          for (int k = 0; k < kMaxD; ++k) {
+            if (k < d) s = __dadd_rn(s, __dmul_rn(th[si * kMaxD + k], t[k]));
+          }
+          v = exp(-s);
+          if (!isfinite(v)) status[slot] = 2;  // GPEMU_SLOT_NONFINITE
+        }
+        factors[(size_t)slot * slot_stride + (size_t)tile * TILE_ELEMS + e] = v;
+      }
+    }
+  }
+}
+
+void launch_assemble(const double* table, const double* theta, const double* y, int n, int d,
+                     double nugget, int NT, const int* slots, int nslots, const double* jitter,
+                     double* factors, size_t slot_stride, double* borders, int* status,
+                     cudaStream_t s) {
+  const int Npad = NT * TILE;
+  border_init_kernel<<<dim3((Npad + 255) / 256 < 32 ? (Npad + 255) / 256 : 32, nslots), 256, 0, s>>>(
+      y, n, Npad, slots, borders, status);
+  dim3 grid(num_tiles(NT), 8);
+  assemble_kernel<<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                       factors, slot_stride, status);
+}
+
+// build_corr_matrix (correlation.hpp:99-146): row-major, strict lower computed
+// once and mirrored.
+__global__ void build_corr_rowmajor_kernel(const double* __restrict__ X, int n, int d,
+                                           const double* __restrict__ theta, double p,
+                                           double nugget, double* __restrict__ R, int* bad) {
+  const int i = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= i; j += gridDim.x * blockDim.x) {
+    if (j == i) {
+      R[(size_t)i * n + i] = __dadd_rn(1.0, nugget);
+      continue;
+    }
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double term = pow_abs(X[(size_t)i * d + k] - X[(size_t)j * d + k], p);
+      s = __dadd_rn(s, __dmul_rn(theta[k], term));
+    }
+    const double v = exp(-s);
+    if (!isfinite(v)) *bad = 1;
+    R[(size_t)i * n + j] = v;
+    R[(size_t)j * n + i] = v;
+  }
+}
+
+void launch_build_corr_rowmajor(const double* X, int n, int d, const double* theta, double p,
+                                double nugget, double* R, int* bad, cudaStream_t s) {
+  dim3 grid((n + 255) / 256, n);
+  build_corr_rowmajor_kernel<<<grid, 256, 0, s>>>(X, n, d, theta, p, nugget, R, bad);
+}
+
+// corr_vector (correlation.hpp:67-91) for N test points: r[j*n + i].
+__global__ void corr_vectors_kernel(const double* __restrict__ Xt, int N,
+                                    const double* __restrict__ X, int n, int d,
+                                    const double* __restrict__ theta, double p,
+                                    double* __restrict__ r, int* bad) {
+  const int j = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < d; ++k) {
+      const double term = pow_abs(Xt[(size_t)j * d + k] - X[(size_t)i * d + k], p);
+      s = __dadd_rn(s, __dmul_rn(theta[k], term));
+    }
+    const double v = exp(-s);
+    if (!isfinite(v)) *bad = 1;
+    r[(size_t)j * n + i] = v;
+  }
+}
+
+void launch_corr_vectors(const double* Xt, int N, const double* X, int n, int d,
+                         const double* theta, double p, double* r, int* bad, cudaStream_t s) {
+  dim3 grid((n + 255) / 256, N);
+  corr_vectors_kernel<<<grid, 256, 0, s>>>(Xt, N, X, n, d, theta, p, r, bad);
+}
+
+}  // namespace gpemu_dev

@@ -1,0 +1,188 @@
+// kernels_misc.cu -- K3 deviance finalisation, layout conversion, single-RHS solves.
+//
+// Reference (relative to /root/reference/proj/include/gpemu/):
+//   factorize_into log-det    backend.hpp:111-113   2 * sum_i log L_ii, sequential, double
+//   dot_accumulate            matrix.hpp:64-69      sequential double dot
+//   eval tail                 likelihood.hpp:124-140
+//   sigma2_hat_from_parts     likelihood.hpp:63-66
+//   solve_lower/upper_into    backend.hpp:129-153
+// The scalar tail keeps the reference's sequential summation order (one thread
+// per dot) and rounds every product/sum separately: it is O(n) and off the
+// critical path, so bitwise-faithful arithmetic costs nothing measurable.
+#include <cuda_runtime.h>
+
+#include <cfloat>
+
+#include "kernels.h"
+#include "layout.cuh"
+
+namespace gpemu_dev {
+
+constexpr int kLogChunk = 2048;
+
+__global__ void __launch_bounds__(256) finalize_kernel(
+    const double* __restrict__ factors, size_t slot_stride, const double* __restrict__ borders,
+    const int* __restrict__ status, const double* __restrict__ jitter, int n, int NT,
+    const int* __restrict__ slots, double* __restrict__ out) {
+  __shared__ double logs[kLogChunk];
+  __shared__ double dots[3];
+  const int slot = slots[blockIdx.x];
+  const int Npad = NT * TILE;
+  const double* fac = factors + (size_t)slot * slot_stride;
+  const double* u = borders + (size_t)slot * 2 * Npad;
+  const double* v = u + Npad;
+  const int st = status[slot];
+  double logsum = 0.0;
+  if (st == 0) {
+    for (int c0 = 0; c0 < n; c0 += kLogChunk) {
+      const int cn = min(kLogChunk, n - c0);
+      for (int q = threadIdx.x; q < cn; q += blockDim.x) {
+        const int i = c0 + q;
+        logs[q] = log(fac[tile_index(i >> 7, i >> 7) * TILE_ELEMS + elem_off(i & 127, i & 127)]);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0)
+        for (int q = 0; q < cn; ++q) logsum = __dadd_rn(logsum, logs[q]);
+      __syncthreads();
+    }
+    if (threadIdx.x < 3) {
+      const double* a = threadIdx.x == 2 ? v : u;
+      const double* b = threadIdx.x == 0 ? u : v;
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+      dots[threadIdx.x] = s;  // 0: utu, 1: vtu (v.u), 2: vtv
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  double* o = out + (size_t)slot * REC_SIZE;
+  const double inf = __longlong_as_double(0x7ff0000000000000LL);
+  o[REC_NEG2] = inf;
+  o[REC_MU] = 0.0;
+  o[REC_SIGMA2] = 0.0;
+  o[REC_JITTER] = 0.0;
+  o[REC_LOGDET] = 0.0;
+  o[REC_UTU] = 0.0;
+  o[REC_VTV] = 0.0;
+  if (st != 0) {
+    o[REC_STATUS] = (double)st;
+    return;
+  }
+  const double log_det = __dmul_rn(2.0, logsum);
+  const double utu = dots[0], vtu = dots[1], vtv = dots[2];
+  o[REC_LOGDET] = log_det;
+  o[REC_UTU] = utu;
+  o[REC_VTV] = vtv;
+  if (!(vtv > 0.0)) {  // likelihood.hpp:127
+    o[REC_STATUS] = 3.0;
+    return;
+  }
+  const double mu = vtu / vtv;
+  const double t1 = __dmul_rn(__dmul_rn(2.0, mu), vtu);
+  const double t2 = __dmul_rn(__dmul_rn(mu, mu), vtv);
+  double s2 = __dadd_rn(__dsub_rn(utu, t1), t2) / (double)n;
+  if (s2 < 0.0) s2 = 0.0;
+  const double qf = __dmul_rn((double)n, s2);
+  const double qf_floored = qf > DBL_MIN ? qf : DBL_MIN;  // likelihood.hpp:134
+  o[REC_NEG2] = __dadd_rn(log_det, __dmul_rn((double)n, log(qf_floored)));
+  o[REC_MU] = mu;
+  o[REC_SIGMA2] = s2;
+  o[REC_JITTER] = jitter[slot];
+  o[REC_STATUS] = 0.0;
+}
+
+void launch_finalize(const double* factors, size_t slot_stride, const double* borders,
+                     const int* status, const double* jitter, int n, int NT, const int* slots,
+                     int nslots, double* out, cudaStream_t s) {
+  finalize_kernel<<<nslots, 256, 0, s>>>(factors, slot_stride, borders, status, jitter, n, NT,
+                                         slots, out);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void rowmajor_to_tiles_kernel(const double* __restrict__ A, int n, double jitter,
+                                         double* __restrict__ tiles) {
+  const int tile = blockIdx.x;
+  int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  while (I * (I + 1) / 2 > tile) --I;
+  const int J = tile - I * (I + 1) / 2;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    int r, c;
+    elem_rc(e, r, c);
+    const int i = I * TILE + r, j = J * TILE + c;
+    double v;
+    if (i >= n || j >= n) {
+      v = (i == j) ? 1.0 : 0.0;
+    } else if (i == j) {
+      v = __dadd_rn(A[(size_t)i * n + i], jitter);
+    } else {
+      v = i > j ? A[(size_t)i * n + j] : A[(size_t)j * n + i];  // lower triangle only
+    }
+    tiles[(size_t)tile * TILE_ELEMS + e] = v;
+  }
+}
+
+void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, double* tiles,
+                              cudaStream_t s) {
+  rowmajor_to_tiles_kernel<<<dim3(num_tiles(NT), 8), 256, 0, s>>>(A, n, jitter, tiles);
+}
+
+__global__ void tiles_to_rowmajor_kernel(const double* __restrict__ tiles, int n,
+                                         double* __restrict__ L) {
+  const int i = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    L[(size_t)i * n + j] =
+        j <= i ? tiles[tile_index(i >> 7, j >> 7) * TILE_ELEMS + elem_off(i & 127, j & 127)] : 0.0;
+  }
+}
+
+void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s) {
+  tiles_to_rowmajor_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(tiles, n, L);
+}
+
+// Column-oriented substitution; per entry the subtraction order matches the
+// reference's row-oriented loop for the forward solve (ascending k).
+__global__ void __launch_bounds__(1024) tri_solve_kernel(const double* __restrict__ tiles, int n,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ x, int upper) {
+  extern __shared__ double w[];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = b[i];
+  __syncthreads();
+  auto Lat = [&](int i, int j) {
+    return tiles[tile_index(i >> 7, j >> 7) * TILE_ELEMS + elem_off(i & 127, j & 127)];
+  };
+  if (!upper) {
+    for (int k = 0; k < n; ++k) {
+      const double xk = w[k] / Lat(k, k);
+      __syncthreads();
+      for (int l = k + 1 + threadIdx.x; l < n; l += blockDim.x)
+        w[l] = __dsub_rn(w[l], __dmul_rn(Lat(l, k), xk));
+      if (threadIdx.x == 0) w[k] = xk;
+      __syncthreads();
+    }
+  } else {
+    for (int k = n - 1; k >= 0; --k) {
+      const double xk = w[k] / Lat(k, k);
+      __syncthreads();
+      for (int l = threadIdx.x; l < k; l += blockDim.x)
+        w[l] = __dsub_rn(w[l], __dmul_rn(Lat(k, l), xk));
+      if (threadIdx.x == 0) w[k] = xk;
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = w[i];
+}
+
+void launch_tri_solve(const double* tiles, int n, int NT, const double* b, double* x, int upper,
+                      cudaStream_t s) {
+  const size_t smem = (size_t)n * sizeof(double);
+  static int configured_for = 0;
+  if ((int)smem > 48 * 1024 && configured_for < (int)smem) {
+    cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(smem < 227 * 1024 ? 227 * 1024 : smem));
+    configured_for = (int)smem;
+  }
+  tri_solve_kernel<<<1, 1024, smem, s>>>(tiles, n, b, x, upper);
+}
+
+}  // namespace gpemu_dev

@@ -1,0 +1,258 @@
+"""GPU parity: the sm_100a path (through the C-ABI) against the oracle and the
+reference-generated golden fixtures.
+
+Gates:
+  * R, corr_vector: elementwise relative <= 1e-14 (libdevice exp/log vs glibc: not bitwise)
+  * per candidate -2logL: |gpu-ref|/|ref| <= max(1e-9, 10 * reference self-discrepancy)
+    (the reference's own `reference` vs `parallel` backends, native build), with the
+    jitter step and the +inf status EQUAL
+  * GA argmin theta-hat and the per-generation trace: bitwise equal
+  * predictions: max|yhat-ref| / max(|yhat|, |y|_inf) <= max(1e-8, 10 * reference self-disc.)
+  * simple engine on identical R: bitwise equal to ReferenceBackend
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def g():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1203_1269_b200 import gpemu
+    return gpemu
+
+
+def rel(a, b):
+    a, b = np.atleast_1d(np.asarray(a, dtype=float)), np.atleast_1d(np.asarray(b, dtype=float))
+    den = np.maximum(np.abs(a), np.abs(b))
+    den[den == 0] = 1.0
+    return float(np.max(np.abs(a - b) / den)) if a.size else 0.0
+
+
+def gate_neg2(got, want, self_disc):
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isinf(got), np.isinf(want)), "+inf status differs"
+    r = np.abs(got[fin] - want[fin]) / np.abs(want[fin])
+    tol = np.maximum(1e-9, 10.0 * self_disc[fin])
+    bad = np.nonzero(r > tol)[0]
+    assert bad.size == 0, f"{bad.size} candidates over gate; worst rel {r.max():.3e}"
+    return float(r.max()) if r.size else 0.0
+
+
+# ---------------------------------------------------------------- correlation
+def test_corr_known_answers(g, ctx):
+    R = g.build_corr_matrix([[0.2, 0.7], [0.2, 0.7]], g.Hyperparameters([3.0, 5.0]), ctx).values
+    assert np.all(R == 1.0)
+    R = g.build_corr_matrix([[0.1], [0.4], [0.9]], g.Hyperparameters([0.0]), ctx).values
+    assert np.all(R == 1.0)
+    R = g.build_corr_matrix([[0.0], [1.0]], g.Hyperparameters([2.0]), ctx).values
+    assert rel(R[0, 1], 0.1353352832366127) < 1e-15
+    r = g.corr_vector([0.5], [[0.0]], g.Hyperparameters([1.0], 2.0), ctx)
+    assert rel(r[0], 0.7788007830714049) < 1e-15
+    with pytest.raises(g.ValidationError):
+        g.corr_vector([0.5], [[0.1, 0.3], [0.6, 0.9]], g.Hyperparameters([1.0, 1.0]), ctx)
+
+
+def test_corr_matches_oracle(g, ctx, orc):
+    rng = np.random.default_rng(7781)
+    for it in range(10):
+        n, d = 2 + int(rng.integers(60)), 1 + int(rng.integers(5))
+        X = rng.random((n, d))
+        th = rng.uniform(0.0, 8.0, d)
+        nug = 0.05 if it % 3 == 0 else 0.0
+        R = g.build_corr_matrix(X, g.Hyperparameters(th, 1.95, nug), ctx).values
+        assert rel(R, orc.build_corr(X, th, 1.95, nug)) < 1e-14
+        assert np.array_equal(R, R.T)
+        assert np.all(np.diag(R) == 1.0 + nug)
+        # corr_vector equals a matrix row minus the nugget, bitwise (test_correlation.cpp:142-162)
+        v = g.corr_vector(X[1], X, g.Hyperparameters(th, 1.95, nug), ctx)
+        row = R[1].copy()
+        row[1] -= nug
+        assert np.array_equal(v, row)
+
+
+# ---------------------------------------------------------------- backend
+@pytest.mark.parametrize("engine", ["simple", "dag"])
+def test_factorize_known_answers(g, engine):
+    be = g.Backend(g.Context(0, engine))
+    f = be.factorize(g.CorrelationMatrix(np.eye(2)))
+    assert f.lower[0, 0] == 1.0 and f.lower[1, 1] == 1.0 and f.lower[1, 0] == 0.0
+    assert f.log_det == 0.0 and f.jitter_used == 0.0
+    f = be.factorize(g.CorrelationMatrix(np.array([[1.0, 0.5], [0.5, 1.0]])))
+    assert f.lower[0, 0] == 1.0 and f.lower[1, 0] == 0.5
+    assert rel(f.lower[1, 1], 0.8660254037844386) < 1e-15
+    assert rel(f.log_det, -0.2876820724517809) < 1e-12
+    u = be.solve_lower(f, [1.0, 1.0])
+    assert u[0] == 1.0 and rel(u[1], 0.5773502691896258) < 1e-15
+    x = be.solve_full(f, [1.0, 1.0])
+    assert rel(x, [2 / 3, 2 / 3]) < 1e-12
+    with pytest.raises(g.NotPositiveDefiniteError):
+        be.factorize(g.CorrelationMatrix(np.array([[1.0, 2.0], [2.0, 1.0]])))
+    Xc = np.array([[0.3, 0.3], [0.3, 0.3], [0.7, 0.1]])
+    R = g.build_corr_matrix(Xc, g.Hyperparameters([2.0, 2.0]), be.ctx)
+    f = be.factorize(R)
+    assert f.jitter_used in (1e-8, 1e-7, 1e-6, 1e-5, 1e-4)
+    LLt = f.lower @ f.lower.T
+    assert np.max(np.abs(np.tril(LLt - R.values - f.jitter_used * np.eye(3)))) <= 1e-8 * 3
+
+
+def test_simple_engine_bitwise_reference_cholesky(g, orc):
+    be = g.Backend(g.Context(0, "simple"))
+    rng = np.random.default_rng(222)
+    for n in (5, 40, 100, 300):
+        X = rng.random((n, 2))
+        R = orc.build_corr(X, rng.uniform(0.3, 5.0, 2) * 10, 1.95)
+        f = be.factorize(g.CorrelationMatrix(R))
+        L, ld, jt = orc.factorize(R, kind=0)
+        assert np.array_equal(f.lower, np.tril(L)) and f.log_det == ld and f.jitter_used == jt
+
+
+@pytest.mark.parametrize("n", [7, 64, 130, 257, 300, 640])
+def test_dag_factorize_reconstruction(g, orc, n):
+    be = g.Backend(g.Context(0, "dag"))
+    rng = np.random.default_rng(n)
+    X = rng.random((n, 3))
+    R = orc.build_corr(X, rng.uniform(0.3, 5.0, 3), 1.95)
+    f = be.factorize(g.CorrelationMatrix(R))
+    L, ld, jt = orc.factorize(R)
+    assert f.jitter_used == jt
+    assert abs(f.log_det - ld) <= 1e-10 * max(1.0, abs(ld))
+    # reconstruction bound (test_backend.cpp:155-174)
+    err = np.max(np.abs(np.tril(f.lower @ f.lower.T - R - jt * np.eye(n))))
+    assert err <= 1e-8 * n
+    # solve round-trip (test_backend.cpp:176-196)
+    x = rng.uniform(-1, 1, n)
+    b = f.lower @ (f.lower.T @ x)
+    assert rel(be.solve_full(f, b), x) < 1e-6
+
+
+# ---------------------------------------------------------------- deviance
+@pytest.mark.parametrize("engine", ["simple", "dag"])
+@pytest.mark.parametrize("name", ["c1", "c1p195"])
+def test_eval_batch_c1_goldens(g, name, engine):
+    z = np.load(os.path.join(GOLD, f"{name}.npz"))
+    be = g.Backend(g.Context(0, engine))
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), float(z["p"]), 0.0, be, max_batch=100)
+    r = ev.eval_batch(z["thetas"])
+    assert np.array_equal(r["jitter"], z["jitter"])
+    gate_neg2(r["neg2"], z["neg2"], z["self_disc"])
+    fin = np.isfinite(z["neg2"])
+    assert rel(r["log_det"][fin], z["log_det"][fin]) < 1e-9
+    ev.close()
+
+
+def test_eval_batch_c2_golden(g, ctx):
+    z = np.load(os.path.join(GOLD, "c2.npz"))
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), 1.95, 0.0, g.Backend(ctx), max_batch=16)
+    r = ev.eval_batch(z["thetas"])
+    assert np.array_equal(r["jitter"], z["jitter"])
+    gate_neg2(r["neg2"], z["neg2"], z["self_disc"])
+    ev.close()
+
+
+def test_batch_invariance(g, ctx):
+    """Same theta in any slot / batch size -> bitwise identical record."""
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), 1.95, 0.0, g.Backend(ctx), max_batch=100)
+    a = ev.eval_batch(z["thetas"])
+    perm = np.random.default_rng(3).permutation(100)
+    b = ev.eval_batch(z["thetas"][perm])
+    c = ev.eval_batch(z["thetas"][17:21])
+    for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+        assert np.array_equal(a[k][perm], b[k]), k
+        assert np.array_equal(a[k][17:21], c[k]), k
+    single = ev.eval(z["thetas"][42])
+    assert single.neg2_log_lik == a["neg2"][42]
+    ev.close()
+
+
+def test_ladder_mixed_batch(g, ctx, orc):
+    """Coincident design points: some thetas need jitter, the ladder reruns only those."""
+    X = np.array([[0.3, 0.3], [0.3, 0.3], [0.7, 0.1], [0.2, 0.9], [0.55, 0.45]])
+    y = np.array([1.0, 1.0, -0.5, 0.25, 0.75])
+    th = np.array([[2.0, 2.0], [0.5, 7.0], [11.0, 0.1], [1e-6, 1e-6]])
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=4)
+    r = ev.eval_batch(th)
+    o = orc.eval_batch(X, y, th, 1.95)
+    assert np.array_equal(r["jitter"], o["jitter"])
+    assert np.array_equal(np.isinf(r["neg2"]), np.isinf(o["neg2"]))
+    assert rel(r["neg2"], o["neg2"]) < 1e-6
+    ev.close()
+
+
+def test_large_n_property_checks(g, ctx, orc):
+    """n=2048 / d=6 at B=4: factor reconstruction and deviance recomputed from the factor."""
+    import torch
+    z = np.load(os.path.join(GOLD, "c2.npz"))
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), 1.95, 0.0, g.Backend(ctx), max_batch=4)
+    r = ev.eval_batch(z["thetas"][:4])
+    for s in range(4):
+        f = ev.last_factor(s)
+        Lt = torch.from_numpy(f.lower).cuda()
+        R = torch.from_numpy(g.build_corr_matrix(z["X"], g.Hyperparameters(z["thetas"][s], 1.95),
+                                                 ctx).values).cuda()
+        err = torch.max(torch.abs(torch.tril(Lt @ Lt.T - R))).item()
+        assert err <= 1e-8 * 2048
+        assert abs(f.log_det - 2 * np.sum(np.log(np.diag(f.lower)))) <= 1e-9 * abs(f.log_det)
+        # deviance from the factor by an independent route (torch triangular solves)
+        y = torch.from_numpy(z["y"]).cuda()[:, None]
+        one = torch.ones_like(y)
+        u = torch.linalg.solve_triangular(Lt, y, upper=False)
+        v = torch.linalg.solve_triangular(Lt, one, upper=False)
+        utu, vtu, vtv = (u * u).sum().item(), (v * u).sum().item(), (v * v).sum().item()
+        mu = vtu / vtv
+        s2 = max(0.0, (utu - 2 * mu * vtu + mu * mu * vtv) / 2048)
+        neg2 = f.log_det + 2048 * np.log(max(2048 * s2, np.finfo(float).tiny))
+        assert abs(neg2 - r["neg2"][s]) <= 1e-9 * abs(neg2) + 1e-12
+    ev.close()
+
+
+# ---------------------------------------------------------------- fit + predict
+def test_fit_c1_argmin_bitwise(g, ctx):
+    z = np.load(os.path.join(GOLD, "c1.npz"))
+    data = g.new_dataset(z["X"], z["y"])
+    cfg = g.FitConfig(ga=g.GaConfig(population=100, generations=20), seed=0, p=2.0)
+    be = g.Backend(ctx)
+    fr = g.fit_gp_detailed(data, cfg, be)
+    assert np.array_equal(np.array(fr.model.params.theta), z["fit_theta"])
+    assert np.array_equal(np.array([r.best_point for r in fr.trace.generations]), z["trace_genes"])
+    assert abs(fr.model.neg2_log_lik - z["fit_neg2"]) <= 1e-9 * abs(z["fit_neg2"])
+    assert fr.jitter_max == z["fit_jitter_max"]
+    led = fr.ledger  # SPEC.md:499 cost model: 2000 / 2000 / 4002
+    assert (led.r_builds, led.factorizations, led.triangular_solves) == (2000, 2000, 4002)
+    yhat, mse = g.predict(fr.model, z["Xt"], with_mse=True)
+    scale = max(np.abs(z["yhat"]).max(), np.abs(z["y"]).max())
+    tol = max(1e-8, 10 * float(z["yhat_self_disc"]))
+    assert np.max(np.abs(yhat - z["yhat"])) / scale <= tol
+    assert np.all(mse >= 0.0)
+
+
+def test_predict_and_mse_vs_oracle(g, ctx, orc):
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    X, y = z["X"], z["y"]
+    th = np.array([3.0, 2.0])
+    m = g.model_at_theta(g.new_dataset(X, y), th, 1.95, 0.0, g.Backend(ctx))
+    mp = orc.eval_batch(X, y, th[None, :], 1.95)
+    assert rel(m.neg2_log_lik, mp["neg2"][0]) < 1e-9
+    R = orc.build_corr(X, th, 1.95)
+    L, ld, jt = orc.factorize(R)
+    alpha = orc.solve_upper(L, orc.solve_lower(L, y - mp["mu"][0]))
+    Xt = z["Xt"][:200]
+    yo = orc.predict(X, th, 1.95, mp["mu"][0], alpha, Xt)
+    yhat, mse = g.predict(m, Xt, with_mse=True)
+    scale = max(np.abs(yo).max(), np.abs(y).max())
+    assert np.max(np.abs(yhat - yo)) / scale <= 1e-8
+    mo = orc.kriging_mse(X, th, 1.95, mp["sigma2"][0], L, Xt)
+    assert np.max(np.abs(mse - mo)) <= 1e-8 * mp["sigma2"][0]
+    # interpolation: yhat at training points reproduces y, MSE ~ 0
+    yt, mt = g.predict(m, X[:20], with_mse=True)
+    assert np.max(np.abs(yt - y[:20])) <= 1e-6 * np.abs(y).max()
+    assert np.all(mt <= 1e-8 * mp["sigma2"][0])
+    with pytest.raises(g.ValidationError):
+        g.predict(m, np.array([[0.5, 1.5]]))
