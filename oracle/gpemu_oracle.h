@@ -96,6 +96,12 @@ int orc_profile_eval_batch(const double* X, const double* y, size_t n, size_t d,
                            double* neg2, double* mu, double* sigma2, double* jitter,
                            double* log_det);
 
+/* Extended-precision (long double) deviance of the reference's double R + jitter:
+ * the "truth" the reference and the device both approximate. */
+int orc_profile_eval_ld(const double* X, const double* y, size_t n, size_t d, double p,
+                        double nugget, const double* thetas, size_t B, const double* jitters,
+                        double* neg2_out);
+
 /* ---- optimizer.hpp + likelihood.hpp fit -------------------------------- */
 typedef struct {
   int population, generations;

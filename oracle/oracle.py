@@ -89,6 +89,8 @@ class Oracle:
                               _dp, _dp, _dp, _dp]
         L.orc_predict.argtypes = [_dp, _sz, _sz, _dp, C.c_double, C.c_double, _dp, _dp, _sz, _dp]
         L.orc_kriging_mse.argtypes = [_dp, _sz, _sz, _dp, C.c_double, C.c_double, _dp, _dp, _sz, _dp]
+        L.orc_profile_eval_ld.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _sz,
+                                          _dp, _dp]
         L.orc_sspe.restype = C.c_double
         L.orc_sspe.argtypes = [_dp, _dp, _sz]
 
@@ -181,6 +183,18 @@ class Oracle:
                                              _ptr(out["jitter"]), _ptr(out["log_det"]))
         if rc != 0:
             raise MemoryError("oracle eval_batch allocation failed")
+        return out
+
+    def eval_truth(self, X, y, thetas, p, jitters, nugget=0.0):
+        """Long-double deviance of the reference's double R + jitter (accuracy yardstick)."""
+        X, y, thetas = _f64(X), _f64(y), _f64(np.atleast_2d(thetas))
+        n, d = X.shape
+        B = thetas.shape[0]
+        jit = _f64(np.broadcast_to(jitters, (B,)))
+        out = np.empty(B)
+        if self.lib.orc_profile_eval_ld(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
+                                        _ptr(jit), _ptr(out)) != 0:
+            raise MemoryError("oracle eval_truth allocation failed")
         return out
 
     def fit(self, X, y, p=1.95, nugget=0.0, lo=1e-6, hi=12.0, population=100, generations=20,

@@ -18,6 +18,7 @@
 //     DIAG(b, j):  C = R(j,j) - sum_{K<j} L(j,K) L(j,K)^T     (DMMA)
 //                  L(j,j) = chol(C)      blocked 16-wide in shared memory
 //                  border rows: [u_j; v_j] = ([y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T) L(j,j)^-T
+//   (every update is applied as a running residual: accumulators start at R)
 //     OFF(b, j, I): C = R(I,j) - sum_{K<j} L(I,K) L(j,K)^T    (DMMA)
 //                  L(I,j) = C L(j,j)^-T  blocked 16-wide (substitution + DMMA updates)
 //   The two forward solves of the reference are the bordered rows [y 1]^T of
@@ -329,12 +330,25 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       const int wm = warp >> 2, wn = warp & 3;
       const int lr = lane >> 2, lc = lane & 3;
       const int brow = tid >> 7, bc = tid & 127;  // border accumulation role (DIAG)
+      // Accumulators start from R(I,j) and the products are SUBTRACTED (negated A
+      // operand, free in DMMA): the running-residual order of the reference's
+      // `v -= L_it * L_jt` (backend.hpp:197-204), which keeps the rounding error
+      // relative to the shrinking residual instead of the growing sum.
+      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
       double acc[8][4][2];
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-      double wacc = 0.0;
+        for (int ni = 0; ni < 4; ++ni) {
+          const int r = wm * 64 + mi * 8 + lr;
+          const int off = wn * 4096 + r * 32 + ((((2 * ni + (lc >> 1)) ^ lr)) << 2) + 2 * (lc & 1);
+          const double2 v = skip ? make_double2(0.0, 0.0)
+                                 : __ldcg(reinterpret_cast<const double2*>(gtile + off));
+          acc[mi][ni][0] = v.x;
+          acc[mi][ni][1] = v.y;
+        }
+      // border rows (DIAG): running residual of [y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T
+      double wacc = (diag && !skip) ? __ldcg(bord + brow * Npad + j * TILE + bc) : 0.0;
 
       for (int q = 0; q < nslab; ++q, ++it) {
         const int stage = it % kStages;
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           const int ko = (ks ^ lr) << 2;
           double av[8], bv[4];
 #pragma unroll
-          for (int mi = 0; mi < 8; ++mi) av[mi] = Aw[mi * 256 + ko];
+          for (int mi = 0; mi < 8; ++mi) av[mi] = -Aw[mi * 256 + ko];
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) bv[ni] = Bw[ni * 256 + ko];
 #pragma unroll
@@ -362,14 +376,14 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           const int K = q >> 2, sq = q & 3;
           const double* ub = bord + brow * Npad + K * TILE + sq * SLAB;
 #pragma unroll 8
-          for (int kk = 0; kk < SLAB; ++kk) wacc += __ldcg(ub + kk) * Bs[slab_off(bc, kk)];
+          for (int kk = 0; kk < SLAB; ++kk) wacc -= __ldcg(ub + kk) * Bs[slab_off(bc, kk)];
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
       consumer_sync();  // every consumer is done reading the stage ring
 
-      // accumulators -> C (tile layout); C = R - acc
+      // accumulators (= R - sum L L^T) -> C (tile layout)
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi)
 #pragma unroll
@@ -379,22 +393,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           *reinterpret_cast<double2*>(C + off) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
         }
       consumer_sync();
-      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
-      if (!skip) {
-        for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers) {
-          const double2 r = __ldcg(reinterpret_cast<const double2*>(gtile + e));
-          double2* cp = reinterpret_cast<double2*>(C + e);
-          const double2 s = *cp;
-          *cp = make_double2(r.x - s.x, r.y - s.y);
-        }
-      }
-      consumer_sync();
 
       if (diag) {
         // ------------------------------ DIAG ------------------------------
         bool ok = !skip;
         if (!skip) {
-          W[brow * TILE + bc] = __ldcg(bord + brow * Npad + j * TILE + bc) - wacc;
+          W[brow * TILE + bc] = wacc;
           for (int kb = 0; kb < 8 && ok; ++kb) {
             const int o = 16 * kb;
             if (warp == 0) {

@@ -8,6 +8,8 @@ time only); the fixtures are committed and travel to the GPU box.
             (GA 100x20) and 1000 test-point predictions
   c1p195.npz  same design, p=1.95 (self-discrepancy stress: near-singular thetas)
   c2.npz    config C2 design (n=2048, d=6, p=1.95, hartman6) with 16 thetas
+Each eval set also stores `self_disc` (the reference's native build: ReferenceBackend vs
+ParallelBackend) and `truth` (long-double deviance of the same double R, oracle/eval_truth).
 """
 import os
 import sys
@@ -16,7 +18,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from oracle.oracle import RefLib, build  # noqa: E402
+from oracle.oracle import Oracle, RefLib, build  # noqa: E402
 
 OUT = os.path.join(ROOT, "tests", "golden")
 
@@ -38,6 +40,7 @@ def self_disc(fast, X, y, th, p):
 def main():
     build()
     ref, fast = RefLib(), RefLib(fast=True)
+    orc = Oracle()
     os.makedirs(OUT, exist_ok=True)
 
     # ---- known answers ------------------------------------------------------
@@ -67,7 +70,10 @@ def main():
         th = ga_thetas(ref, 2, 100)
         ev = ref.eval_batch(X, y, th, p)
         disc = self_disc(fast, X, y, th, p)
+        truth = orc.eval_truth(X, y, th, p, ev["jitter"])
         fit = ref.fit(X, y, p=p, population=100, generations=20, seed=0)
+        opt = ref.eval_batch(X, y, fit["theta"][None, :], p)
+        fit_truth = orc.eval_truth(X, y, fit["theta"][None, :], p, opt["jitter"])[0]
         Xt = ref.maximin_lhd(1000, 2, 11, 10000)
         mp = ref.model_predict(X, y, fit["theta"], p, 0.0, Xt)
         # reference self-discrepancy of the predictions (native build, reference vs parallel)
@@ -77,7 +83,8 @@ def main():
         yhat_self_disc = np.abs(ya - yb).max() / yscale
         np.savez(os.path.join(OUT, f"{name}.npz"), X=X, y=y, p=p, thetas=th,
                  neg2=ev["neg2"], mu=ev["mu"], sigma2=ev["sigma2"], jitter=ev["jitter"],
-                 log_det=ev["log_det"], self_disc=disc, fit_theta=fit["theta"], fit_neg2=fit["neg2"],
+                 log_det=ev["log_det"], self_disc=disc, truth=truth, fit_theta=fit["theta"],
+                 fit_neg2=fit["neg2"], fit_truth=fit_truth,
                  fit_mu=fit["mu"], fit_sigma2=fit["sigma2"], fit_jitter_max=fit["jitter_max"],
                  fit_alpha=fit["alpha"], trace_best=fit["trace_best"],
                  trace_genes=fit["trace_genes"], Xt=Xt, yhat=mp["yhat"],
@@ -92,8 +99,10 @@ def main():
     th = ga_thetas(ref, 6, 64)[:16]
     ev = ref.eval_batch(X, y, th, 1.95, threads=8)
     disc = self_disc(fast, X, y, th, 1.95)
+    truth = orc.eval_truth(X, y, th, 1.95, ev["jitter"])
     np.savez(os.path.join(OUT, "c2.npz"), X=X, y=y, p=1.95, thetas=th, neg2=ev["neg2"], mu=ev["mu"],
-             sigma2=ev["sigma2"], jitter=ev["jitter"], log_det=ev["log_det"], self_disc=disc)
+             sigma2=ev["sigma2"], jitter=ev["jitter"], log_det=ev["log_det"], self_disc=disc,
+             truth=truth)
     print("c2 done")
 
 
