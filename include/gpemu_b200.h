@@ -106,6 +106,16 @@ int gpemu_eval_batch_device(gpemu_plan* plan, const double* d_theta, size_t B, d
 int gpemu_plan_last_factor(gpemu_plan* plan, size_t slot, double* L_out, double* log_det,
                            double* jitter_used);
 
+/* Per-phase device timing (CUDA events on the plan's stream) for roofline
+ * accounting: phase 0 = correlation assembly (K1), 1 = Cholesky engine (K2),
+ * 2 = deviance finalisation (K3). Enabling clears previous marks. */
+int gpemu_plan_set_profiling(gpemu_plan* plan, int enable);
+int gpemu_plan_phase_ms(gpemu_plan* plan, int phase, double* total_ms, int* launches);
+/* Diagnostics: per-CTA phase cycle counters of the DAG engine ([num_sms][16], see
+ * kernels_chol.cu PR_*). enable=1 (re)arms and zeroes them; out (nullable) receives the
+ * counters accumulated since; enable=0 disarms. */
+int gpemu_plan_dag_profile(gpemu_plan* plan, int enable, uint64_t* out, size_t out_len);
+
 /* ---- optimizer.hpp / likelihood.hpp fit ------------------------------- */
 typedef struct {
   int population;       /* GaConfig::population (100) */

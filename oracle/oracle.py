@@ -272,6 +272,8 @@ class RefLib:
         L.ref_solve.argtypes = [_dp, _sz, _dp, C.c_int, _dp]
         L.ref_eval_batch.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _sz, cs,
                                      C.c_uint, _dp, _dp, _dp, _dp, _dp]
+        L.ref_eval_batch_timed.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _sz,
+                                           cs, C.c_uint, _dp, _dp, _dp]
         L.ref_fit.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _dp, C.c_int,
                               C.c_int, _u64, cs, C.c_uint, _dp, _dp, _dp, _dp, _dp]
         L.ref_model_predict.argtypes = [_dp, _dp, _sz, _sz, _dp, C.c_double, C.c_double, cs,
@@ -347,6 +349,18 @@ class RefLib:
                                             _ptr(out["mu"]), _ptr(out["sigma2"]),
                                             _ptr(out["jitter"]), _ptr(out["log_det"])))
         return out
+
+    def eval_batch_timed(self, X, y, thetas, p, nugget=0.0, backend="parallel", threads=0):
+        """-> (neg2, seconds_plan, seconds_evals); threads=0 = hardware_concurrency."""
+        X, y, thetas = _f64(X), _f64(y), _f64(np.atleast_2d(thetas))
+        n, d = X.shape
+        B = thetas.shape[0]
+        neg2 = np.empty(B)
+        sp, se = C.c_double(), C.c_double()
+        self._check(self.lib.ref_eval_batch_timed(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
+                                                  backend.encode(), threads, _ptr(neg2),
+                                                  C.byref(sp), C.byref(se)))
+        return neg2, sp.value, se.value
 
     def fit(self, X, y, p=1.95, nugget=0.0, lo=1e-6, hi=12.0, population=100, generations=20,
             seed=0, backend="parallel", threads=1):

@@ -5,6 +5,7 @@
 // into oracle/_ref/libgpemu_ref*.so. Used (a) to pin the C restatement
 // oracle/gpemu_oracle.c, (b) to generate tests/golden fixtures, and (c) as the
 // timed CPU baseline in bench.py (cpu_baseline kind "reference").
+#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -164,6 +165,26 @@ REF_API int ref_eval_batch(const double* X, const double* y, std::size_t n, std:
     if (jitter) jitter[b] = r.jitter_used;
     if (log_det) log_det[b] = std::isfinite(r.neg2_log_lik) ? ev.last_factor().log_det : 0.0;
   }
+  return 0;
+  REF_CATCH
+}
+
+// Timed ProfileEvaluator::eval loop: plan construction and the B evaluations are
+// timed separately (steady_clock), as BASELINE.md 3 prescribes for evals/s.
+REF_API int ref_eval_batch_timed(const double* X, const double* y, std::size_t n, std::size_t d,
+                                 double p, double nugget, const double* thetas, std::size_t B,
+                                 const char* backend, unsigned threads, double* neg2,
+                                 double* seconds_plan, double* seconds_evals) {
+  REF_TRY
+  auto be = make_backend<double>(backend, threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  const auto t0 = std::chrono::steady_clock::now();
+  ProfileEvaluator<double> ev(data, p, nugget, *be);
+  const auto t1 = std::chrono::steady_clock::now();
+  for (std::size_t b = 0; b < B; ++b) neg2[b] = ev.eval(std::span<const double>(thetas + b * d, d)).neg2_log_lik;
+  const auto t2 = std::chrono::steady_clock::now();
+  *seconds_plan = std::chrono::duration<double>(t1 - t0).count();
+  *seconds_evals = std::chrono::duration<double>(t2 - t1).count();
   return 0;
   REF_CATCH
 }

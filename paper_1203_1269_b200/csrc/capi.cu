@@ -143,12 +143,40 @@ struct gpemu_plan {
   int epoch = 0;
   DevBuf<double> X, y, table, factors, borders, theta, jitter, out;
   DevBuf<int> status, slots, flags, counter, error;
+  DevBuf<unsigned long long> dag_prof;  // optional DAG phase counters
   std::vector<double> h_jitter;
   std::vector<int> h_slots, h_status_all;
   std::vector<double> h_out;
   size_t last_B = 0;
   std::vector<int> last_ladder;  // ladder step per slot of the last batch (-1: failed)
   uint64_t r_builds = 0, factorizations = 0, solves = 0;
+  // optional per-phase CUDA-event timing on the plan's stream (bench roofline)
+  bool profile = false;
+  struct Mark {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Mark> marks;
+  void mark_begin(int kind) {
+    if (!profile) return;
+    Mark m{kind, nullptr, nullptr};
+    cudaEventCreate(&m.a);
+    cudaEventCreate(&m.b);
+    cudaEventRecord(m.a, ctx->stream);
+    marks.push_back(m);
+  }
+  void mark_end() {
+    if (!profile) return;
+    cudaEventRecord(marks.back().b, ctx->stream);
+  }
+  void clear_marks() {
+    for (auto& m : marks) {
+      cudaEventDestroy(m.a);
+      cudaEventDestroy(m.b);
+    }
+    marks.clear();
+  }
+  ~gpemu_plan() { clear_marks(); }
 };
 
 struct gpemu_model {
@@ -175,6 +203,7 @@ void run_chol(gpemu_plan* pl, int nact) {
   a.epoch = ++pl->epoch;
   a.status = pl->status.p;
   a.error = pl->error.p;
+  a.prof = pl->dag_prof.p;
   if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
     launch_chol_simple(a, pl->ctx->stream);
   } else {
@@ -206,12 +235,18 @@ int run_batch(gpemu_plan* pl, size_t B) {
     std::copy(active.begin(), active.end(), pl->h_slots.begin());
     ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), nact * sizeof(int), cudaMemcpyHostToDevice, s),
        "H2D slots");
+    pl->mark_begin(0);
     launch_assemble(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
                     pl->slots.p, nact, pl->jitter.p, pl->factors.p, pl->slot_stride,
                     pl->borders.p, pl->status.p, s);
+    pl->mark_end();
+    pl->mark_begin(1);
     run_chol(pl, nact);
+    pl->mark_end();
+    pl->mark_begin(2);
     launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
                     pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+    pl->mark_end();
     pl->ctx->launches += 4;
     ck(cudaGetLastError(), "kernel launch");
     ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, B * sizeof(int), cudaMemcpyDeviceToHost, s),
@@ -631,6 +666,51 @@ int gpemu_eval_batch(gpemu_plan* pl, const double* theta, size_t B, double* neg2
     if (log_det) log_det[b] = r[REC_LOGDET];
     if (slot_status) slot_status[b] = (int)r[REC_STATUS];
   }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_plan_set_profiling(gpemu_plan* pl, int enable) {
+  if (!pl) return set_error(GPEMU_VALIDATION, "null plan");
+  cudaStreamSynchronize(pl->ctx->stream);
+  pl->clear_marks();
+  pl->profile = enable != 0;
+  return GPEMU_OK;
+}
+
+int gpemu_plan_phase_ms(gpemu_plan* pl, int phase, double* total_ms, int* launches) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !total_ms) return set_error(GPEMU_VALIDATION, "null argument");
+  ck(cudaStreamSynchronize(pl->ctx->stream), "phase_ms");
+  double t = 0.0;
+  int c = 0;
+  for (auto& m : pl->marks) {
+    if (m.kind != phase) continue;
+    float ms = 0.0f;
+    ck(cudaEventElapsedTime(&ms, m.a, m.b), "cudaEventElapsedTime");
+    t += ms;
+    ++c;
+  }
+  *total_ms = t;
+  if (launches) *launches = c;
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_plan_dag_profile(gpemu_plan* pl, int enable, uint64_t* out, size_t out_len) {
+  GPEMU_GUARD_BEGIN
+  if (!pl) return set_error(GPEMU_VALIDATION, "null plan");
+  const size_t len = (size_t)pl->ctx->num_sms * 16;
+  if (out && pl->dag_prof.p) {
+    ck(cudaStreamSynchronize(pl->ctx->stream), "dag_profile");
+    ck(cudaMemcpy(out, pl->dag_prof.p, std::min(out_len, len) * sizeof(uint64_t), cudaMemcpyDeviceToHost),
+       "D2H prof");
+  }
+  if (enable && !pl->dag_prof.p) {
+    pl->dag_prof.alloc(len);
+  }
+  if (enable) ck(cudaMemset(pl->dag_prof.p, 0, len * sizeof(uint64_t)), "memset prof");
+  if (!enable) pl->dag_prof.free();
   return GPEMU_OK;
   GPEMU_GUARD_END
 }

@@ -39,6 +39,7 @@ struct DagLaunch {
   int epoch;
   int* status;     // [slot]
   int* error;      // deadlock / timeout word
+  unsigned long long* prof = nullptr;  // optional [grid][16] phase cycle counters
 };
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s);
 void launch_chol_simple(const DagLaunch& a, cudaStream_t s);

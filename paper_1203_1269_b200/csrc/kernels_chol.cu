@@ -114,13 +114,12 @@ void launch_chol_simple(const DagLaunch& a, cudaStream_t s) {
 namespace {
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;  // 256
-constexpr int kThreads = kConsumers + 32;        // + producer warp
+constexpr int kThreads = kConsumers;             // thread 0 also issues the TMA loads
 constexpr int kStages = 3;
 constexpr int kSlabBytes = SLAB_ELEMS * 8;              // 32 KB
 constexpr int kStageBytes = 2 * kSlabBytes;             // A + B slab
 constexpr int kOffStages = 0;                           // [0, 192K)
 constexpr int kOffC = 0;                                // epilogue tile [0, 128K)
-constexpr int kOffStrip = 128 * 1024;                   // 2 x 32 KB [128K, 192K)
 constexpr int kOffBar = kStages * kStageBytes;          // 192K: mbarriers
 constexpr int kOffW = kOffBar + 256;                    // border w: 2 x 128 doubles
 constexpr int kOffMisc = kOffW + 2 * TILE * 8;          // task scalars
@@ -155,6 +154,30 @@ __device__ __forceinline__ void publish_flag(int* flag, int epoch) {
   st_release_gpu(flag, epoch);
 }
 
+// Optional per-CTA phase cycle counters (DagLaunch::prof, null in production).
+enum {
+  PR_TICKET = 0, PR_GEMM, PR_ACC_STORE, PR_POTRF, PR_DIAG_STORE, PR_BORDER, PR_OFF_WAIT, PR_TRSM,
+  PR_OFF_STORE, PR_TASK_END, PR_PROD_FLAGS, PR_PROD_EMPTY, PR_N_DIAG, PR_N_OFF, PR_SLABS, PR_TOTAL,
+  PR_COUNT
+};
+struct Prof {
+  unsigned long long* p;
+  long long last;
+  __device__ __forceinline__ void start() {
+    if (p) last = clock64();
+  }
+  __device__ __forceinline__ void lap(int k) {
+    if (p) {
+      const long long now = clock64();
+      p[k] += (unsigned long long)(now - last);
+      last = now;
+    }
+  }
+  __device__ __forceinline__ void add(int k, unsigned long long v) {
+    if (p) p[k] += v;
+  }
+};
+
 // Task decode (see header comment): ticket -> (bpos, j, I).
 __device__ __forceinline__ void decode_task(int t, int B, int NT, int& bpos, int& j, int& I) {
   if (t < B) {
@@ -184,6 +207,12 @@ __device__ __forceinline__ void decode_task(int t, int B, int NT, int& bpos, int
     j = jj;
     I = jj + pos;
   }
+}
+
+// Offset (tile layout) of the double pair (row r, cols 8 ni + 2 lc + {0,1}) held by a
+// DMMA accumulator fragment.
+__device__ __forceinline__ int acc_off(int r, int ni, int lc) {
+  return ((ni >> 2) << 12) + r * 32 + (((2 * (ni & 3) + (lc >> 1)) ^ (r & 7)) << 2) + 2 * (lc & 1);
 }
 
 // C tile accessors in shared memory (tile layout).
@@ -249,8 +278,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* empty = full + kStages;
+  uint64_t* ljj_bar = empty + kStages;  // L(j,j) bulk load for the OFF-task TRSM
   double* C = reinterpret_cast<double*>(smem + kOffC);
-  double* strip = reinterpret_cast<double*>(smem + kOffStrip);
   double* W = reinterpret_cast<double*>(smem + kOffW);
   Misc* misc = reinterpret_cast<Misc*>(smem + kOffMisc);
 
@@ -267,13 +296,18 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], kConsumerWarps);
     }
+    mbar_init(ljj_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
 
   uint32_t it = 0;  // slab iteration counter, advanced identically by both roles
+  uint32_t ljj_phase = 0;  // uses of ljj_bar (consumers)
+  Prof pr{(a.prof && tid == 0) ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr, 0};
+  const long long t_begin = clock64();
+  pr.start();
   while (true) {
-    if (tid == kConsumers) {
+    if (tid == 0) {
       const int t = atomicAdd(a.counter, 1);
       misc->ticket = t;
       if (t < ntasks) {
@@ -286,6 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     __syncthreads();
     const int t = misc->ticket;
     if (t >= ntasks) break;
+    if (tid == 0) pr.lap(PR_TICKET);
     int bpos, j, I;
     decode_task(t, B, NT, bpos, j, I);
     const bool diag = (I == j);
@@ -296,52 +331,24 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     int* flags = a.flags + (size_t)slot * fstride;  // flags[I*NT + J], border row I = NT
     const int nslab = skip ? 0 : SLABS_PER_TILE * j;
 
-    if (warp == kConsumerWarps) {
-      // ------------------------------ producer ------------------------------
-      if (lane == 0) {
-        for (int q = 0; q < nslab; ++q, ++it) {
-          const int K = q >> 2, sq = q & 3;
-          if (sq == 0) {
-            wait_flag(&flags[j * NT + K], epoch, a.error);
-            if (diag) {
-              wait_flag(&flags[NT * NT + K], epoch, a.error);
-            } else {
-              wait_flag(&flags[I * NT + K], epoch, a.error);
-            }
-            fence_proxy_async_global();
-          }
-          const int stage = it % kStages;
-          const uint32_t round = it / kStages;
-          if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
-          unsigned char* dst = smem + kOffStages + stage * kStageBytes;
-          mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
-          bulk_g2s(dst, fac + tile_index(I, K) * TILE_ELEMS + sq * SLAB_ELEMS, kSlabBytes,
-                   &full[stage]);
-          if (!diag) {
-            bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
-                     kSlabBytes, &full[stage]);
-          }
-        }
-      } else {
-        it += nslab;
-      }
-    } else {
+    {
       // ------------------------------ consumers -----------------------------
-      const int wm = warp >> 2, wn = warp & 3;
+      // Warp w owns rows [16w, 16w+16) of the 128x128 tile (two m8 tiles x sixteen n8
+      // tiles): the B operand is shared by all warps through shared memory, and every
+      // row of the result stays in one warp, so the OFF-task TRSM needs no block barrier.
       const int lr = lane >> 2, lc = lane & 3;
       const int brow = tid >> 7, bc = tid & 127;  // border accumulation role (DIAG)
+      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
       // Accumulators start from R(I,j) and the products are SUBTRACTED (negated A
       // operand, free in DMMA): the running-residual order of the reference's
       // `v -= L_it * L_jt` (backend.hpp:197-204), which keeps the rounding error
       // relative to the shrinking residual instead of the growing sum.
-      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
-      double acc[8][4][2];
+      double acc[2][16][2];
 #pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int r = wm * 64 + mi * 8 + lr;
-          const int off = wn * 4096 + r * 32 + ((((2 * ni + (lc >> 1)) ^ lr)) << 2) + 2 * (lc & 1);
+        for (int ni = 0; ni < 16; ++ni) {
+          const int off = acc_off(16 * warp + 8 * mi + lr, ni, lc);
           const double2 v = skip ? make_double2(0.0, 0.0)
                                  : __ldcg(reinterpret_cast<const double2*>(gtile + off));
           acc[mi][ni][0] = v.x;
@@ -350,29 +357,63 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // border rows (DIAG): running residual of [y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T
       double wacc = (diag && !skip) ? __ldcg(bord + brow * Npad + j * TILE + bc) : 0.0;
 
+      // Thread 0 doubles as the TMA producer, kStages-1 slabs ahead of the math.
+      auto issue = [&](int p, uint32_t itp) {
+        const int K = p >> 2, sq = p & 3;
+        if (sq == 0) {
+          pr.start();
+          wait_flag(&flags[j * NT + K], epoch, a.error);
+          if (diag) {
+            wait_flag(&flags[NT * NT + K], epoch, a.error);
+          } else {
+            wait_flag(&flags[I * NT + K], epoch, a.error);
+          }
+          fence_proxy_async_global();
+          pr.lap(PR_PROD_FLAGS);
+        }
+        const int stage = itp % kStages;
+        const uint32_t round = itp / kStages;
+        pr.start();
+        if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
+        pr.lap(PR_PROD_EMPTY);
+        unsigned char* dst = smem + kOffStages + stage * kStageBytes;
+        mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
+        bulk_g2s(dst, fac + tile_index(I, K) * TILE_ELEMS + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
+        if (!diag)
+          bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
+                   kSlabBytes, &full[stage]);
+      };
+      if (tid == 0) {
+        const long long tsave = pr.last;
+        for (int p = 0; p < kStages - 1 && p < nslab; ++p) issue(p, it + p);
+        pr.last = tsave;
+      }
       for (int q = 0; q < nslab; ++q, ++it) {
+        if (tid == 0 && q + kStages - 1 < nslab) {
+          const long long tsave = pr.last;
+          issue(q + kStages - 1, it + kStages - 1);
+          pr.last = tsave;
+        }
         const int stage = it % kStages;
         const uint32_t round = it / kStages;
         mbar_wait(&full[stage], round & 1);
         const double* As = reinterpret_cast<const double*>(smem + kOffStages + stage * kStageBytes);
         const double* Bs = diag ? As : As + SLAB_ELEMS;
-        const double* Aw = As + (wm * 64 + lr) * 32 + lc;
-        const double* Bw = Bs + (wn * 32 + lr) * 32 + lc;
+        const double* Aw = As + (16 * warp + lr) * 32 + lc;
+        const double* Bw = Bs + lr * 32 + lc;
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const int ko = (ks ^ lr) << 2;
-          double av[8], bv[4];
+          const double a0 = -Aw[ko], a1 = -Aw[256 + ko];
 #pragma unroll
-          for (int mi = 0; mi < 8; ++mi) av[mi] = -Aw[mi * 256 + ko];
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni) bv[ni] = Bw[ni * 256 + ko];
-#pragma unroll
-          for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], av[mi], bv[ni]);
+          for (int ni = 0; ni < 16; ++ni) {
+            const double b = Bw[ni * 256 + ko];
+            dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
+            dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
+          }
         }
         if (diag) {
-          // border rows: wacc += sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk]
+          // border rows: wacc -= sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk]
           const int K = q >> 2, sq = q & 3;
           const double* ub = bord + brow * Npad + K * TILE + sq * SLAB;
 #pragma unroll 8
@@ -382,20 +423,23 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (lane == 0) mbar_arrive(&empty[stage]);
       }
       consumer_sync();  // every consumer is done reading the stage ring
-
-      // accumulators (= R - sum L L^T) -> C (tile layout)
-#pragma unroll
-      for (int mi = 0; mi < 8; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int r = wm * 64 + mi * 8 + lr;
-          const int off = wn * 4096 + r * 32 + ((((2 * ni + (lc >> 1)) ^ lr)) << 2) + 2 * (lc & 1);
-          *reinterpret_cast<double2*>(C + off) = make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-        }
-      consumer_sync();
+      if (tid == 0) {
+        pr.lap(PR_GEMM);
+        pr.add(PR_SLABS, nslab);
+        pr.add(diag ? PR_N_DIAG : PR_N_OFF, 1);
+      }
 
       if (diag) {
         // ------------------------------ DIAG ------------------------------
+        // accumulators (= R - sum L L^T) -> C (tile layout)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 16; ++ni)
+            *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, ni, lc)) =
+                make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        consumer_sync();
+        if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
         if (!skip) {
           W[brow * TILE + bc] = wacc;
@@ -434,13 +478,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           }
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
         }
+        if (tid == 0) pr.lap(PR_POTRF);
         // L(j,j) -> HBM, then publish
         if (ok) {
           for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
             __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
         }
         consumer_sync();
-        if (tid == 0) publish_flag(&flags[j * NT + j], epoch);
+        if (tid == 0) {
+          publish_flag(&flags[j * NT + j], epoch);
+          pr.lap(PR_DIAG_STORE);
+        }
         // border solve: [u_j; v_j] = w L(j,j)^-T (column-oriented substitution)
         if (ok && warp < 2) {
           double* w = W + warp * TILE;
@@ -454,57 +502,120 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           for (int l = lane; l < TILE; l += 32) __stcg(bord + warp * Npad + j * TILE + l, w[l]);
         }
         consumer_sync();
-        if (tid == 0) publish_flag(&flags[NT * NT + j], epoch);
+        if (tid == 0) {
+          publish_flag(&flags[NT * NT + j], epoch);
+          pr.lap(PR_BORDER);
+        }
       } else {
         // ------------------------------ OFF -------------------------------
-        if (tid == 0) wait_flag(&flags[j * NT + j], epoch, a.error);
-        consumer_sync();
+        // L(I,j) = C L(j,j)^-T. L(j,j) arrives by TMA into the (now idle) stage ring;
+        // each warp then solves its own 16 rows in registers, 16 columns at a time:
+        // (a) in-block substitution (quad shuffles), (b) DMMA update of the columns to
+        // the right, (c) store the finished block, (d) rotate the accumulator window.
+        if (!skip) {
+          if (tid == 0) {
+            wait_flag(&flags[j * NT + j], epoch, a.error);
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
+            const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
+#pragma unroll
+            for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
+              bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, ljj_bar);
+          }
+          mbar_wait(ljj_bar, ljj_phase & 1);
+          ++ljj_phase;
+        }
+        if (tid == 0) pr.lap(PR_OFF_WAIT);
         const bool run = !skip && *((volatile int*)&a.status[slot]) == 0;
         if (run) {
-          const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
+          const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
+          // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
+          // a*r + one FMA correction (division rounding as in backend.hpp:206)
+          double* rinv = W;
+          if (tid < TILE) rinv[tid] = 1.0 / Ls[elem_off(tid, tid)];
+          consumer_sync();
+          const int qbase = lane & ~3;
           for (int cb = 0; cb < 8; ++cb) {
-            const int s = cb >> 1;
-            double* buf = strip + (s & 1) * SLAB_ELEMS;
-            if ((cb & 1) == 0) {
-              for (int e = 2 * tid; e < SLAB_ELEMS; e += 2 * kConsumers)
-                *reinterpret_cast<double2*>(buf + e) =
-                    __ldcg(reinterpret_cast<const double2*>(Ljj + s * SLAB_ELEMS + e));
-              consumer_sync();
-            }
             const int o = 16 * cb;
-            const int ko = o - 32 * s;  // column offset inside the slab
-            // (a) 16-column substitution, one row per thread
-            if (tid < TILE) {
-              const int r = tid;
-              double x[16];
+            // (a) columns o..o+15 live in acc[mi][0..1] (rotated window)
 #pragma unroll
-              for (int c = 0; c < 16; ++c) x[c] = Cs(C, r, o + c);
+            for (int c = 0; c < 16; ++c) {
+              const int nsub = c >> 3, q = (c & 7) >> 1, e = c & 1;
+              const double rcc = rinv[o + c];
+              const double lcc = Ls[elem_off(o + c, o + c)];
 #pragma unroll
-              for (int c = 0; c < 16; ++c) {
+              for (int mi = 0; mi < 2; ++mi) {
+                // quotient a / L_cc: reciprocal estimate + one FMA residual correction
+                // (the rounding of a true division, without the DDIV call sequence)
+                const double av0 = acc[mi][nsub][e];
+                const double x0 = av0 * rcc;
+                double x = fma(fma(-x0, lcc, av0), rcc, x0);
+                x = __shfl_sync(0xffffffffu, x, qbase | q);
+                if (lc == q) acc[mi][nsub][e] = x;
 #pragma unroll
-                for (int tt = 0; tt < c; ++tt) x[c] -= x[tt] * buf[slab_off(o + c, ko + tt)];
-                x[c] = x[c] / buf[slab_off(o + c, ko + c)];
+                for (int ns2 = 0; ns2 < 2; ++ns2)
+#pragma unroll
+                  for (int e2 = 0; e2 < 2; ++e2) {
+                    const int c2 = 8 * ns2 + 2 * lc + e2;
+                    if (c2 > c) acc[mi][ns2][e2] -= x * Ls[elem_off(o + c2, o + c)];
+                  }
+              }
+            }
+            // (b) acc[:, 2..] -= X_block * L(j,j)[rows right of the block, block cols]^T
+            if (cb < 7) {
+              double av[2][4];
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks) {
+                const int src = qbase | (2 * (ks & 1) + (lc >> 1));
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi) {
+                  const double v0 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][0], src);
+                  const double v1 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][1], src);
+                  av[mi][ks] = -((lc & 1) ? v1 : v0);
+                }
               }
 #pragma unroll
-              for (int c = 0; c < 16; ++c) Cs(C, r, o + c) = x[c];
+              for (int nb = 2; nb < 16; ++nb) {
+                if (nb < 16 - 2 * cb) {
+                  const int nrow = o + 8 * nb + lr;  // row of L(j,j) = output column
+#pragma unroll
+                  for (int ks = 0; ks < 4; ++ks) {
+                    const double b = Ls[elem_off(nrow, o + 4 * ks + lc)];
+                    dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
+                    dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
+                  }
+                }
+              }
             }
-            consumer_sync();
-            // (b) C[:, >= o+16] -= X[:, o:o+16] * L(j,j)[>= o+16, o:o+16]^T
-            if (cb < 7) {
-              warp_update16(C, warp, lane, o, (o + 16) >> 3, 15,
-                            [&](int row, int k) { return buf[slab_off(row, k - 32 * s)]; });
-            }
-            consumer_sync();
+            // (c) the block is final: store it
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int nsub = 0; nsub < 2; ++nsub)
+                __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, 2 * cb + nsub, lc)),
+                       make_double2(acc[mi][nsub][0], acc[mi][nsub][1]));
+            // (d) rotate the window by one 16-column block
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int ni = 0; ni < 14; ++ni) {
+                acc[mi][ni][0] = acc[mi][ni + 2][0];
+                acc[mi][ni][1] = acc[mi][ni + 2][1];
+              }
           }
-          for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
-            __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
+          if (tid == 0) pr.lap(PR_TRSM);
         }
         consumer_sync();
-        if (tid == 0) publish_flag(&flags[I * NT + j], epoch);
+        if (tid == 0) {
+          publish_flag(&flags[I * NT + j], epoch);
+          pr.lap(PR_OFF_STORE);
+        }
       }
     }
     __syncthreads();
+    if (tid == 0) pr.lap(PR_TASK_END);
   }
+  if (tid == 0) pr.add(PR_TOTAL, (unsigned long long)(clock64() - t_begin));
 }
 }  // namespace
 

@@ -68,6 +68,7 @@ __global__ void border_init_kernel(const double* __restrict__ y, int n, int Npad
 }
 
 constexpr int kAsmSlotChunk = 64;
+constexpr int kSlotILP = 4;
 
 __global__ void __launch_bounds__(256) assemble_kernel(
     const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
@@ -87,9 +88,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   for (int c0 = 0; c0 < nslots; c0 += kAsmSlotChunk) {
     const int cn = min(kAsmSlotChunk, nslots - c0);
     __syncthreads();
-    for (int q = threadIdx.x; q < cn * d; q += blockDim.x) {
+    for (int q = threadIdx.x; q < kAsmSlotChunk * d; q += blockDim.x) {
       const int si = q / d, k = q - si * d;
-      th[si * kMaxD + k] = theta[(size_t)slots[c0 + si] * d + k];
+      th[si * kMaxD + k] = si < cn ? theta[(size_t)slots[c0 + si] * d + k] : 0.0;
     }
     for (int q = threadIdx.x; q < cn; q += blockDim.x) sl[q] = slots[c0 + q];
     __syncthreads();
@@ -102,23 +103,38 @@ __global__ void __launch_bounds__(256) assemble_kernel(
 #pragma unroll
       for (int k = 0; k < kMaxD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
       const bool pad = i >= n || j >= n;
-      for (int si = 0; si < cn; ++si) {
-        const int slot = sl[si];
-        double v;
-        if (pad) {
-          v = (i == j) ? 1.0 : 0.0;
-        } else if (i == j) {
-          v = __dadd_rn(diag_base, jitter[slot]);  // backend.hpp:107-109
-        } else {
-          double s = 0.0;
-#pragma unroll
-          for (int k = 0; k < kMaxD; ++k) {
-            if (k < d) s = __dadd_rn(s, __dmul_rn(th[si * kMaxD + k], t[k]));
-          }
-          v = exp(-s);
-          if (!isfinite(v)) status[slot] = 2;  // GPEMU_SLOT_NONFINITE
+      double* dst = factors + (size_t)tile * TILE_ELEMS + e;
+      if (pad || i == j) {
+        for (int si = 0; si < cn; ++si) {
+          const int slot = sl[si];
+          dst[(size_t)slot * slot_stride] =
+              pad ? (i == j ? 1.0 : 0.0) : __dadd_rn(diag_base, jitter[slot]);  // backend.hpp:107-109
         }
-        factors[(size_t)slot * slot_stride + (size_t)tile * TILE_ELEMS + e] = v;
+        continue;
+      }
+      // kSlotILP independent candidates per pass: their sequential k-sums and exps
+      // interleave, hiding the FP64 dependency-chain latency.
+      for (int s0 = 0; s0 < cn; s0 += kSlotILP) {
+        double s[kSlotILP];
+#pragma unroll
+        for (int q = 0; q < kSlotILP; ++q) s[q] = 0.0;
+#pragma unroll
+        for (int k = 0; k < kMaxD; ++k) {
+          if (k < d) {
+#pragma unroll
+            for (int q = 0; q < kSlotILP; ++q)
+              s[q] = __dadd_rn(s[q], __dmul_rn(th[(s0 + q) * kMaxD + k], t[k]));
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < kSlotILP; ++q) {
+          if (s0 + q < cn) {
+            const int slot = sl[s0 + q];
+            const double v = exp(-s[q]);
+            if (!isfinite(v)) status[slot] = 2;  // GPEMU_SLOT_NONFINITE
+            dst[(size_t)slot * slot_stride] = v;
+          }
+        }
       }
     }
   }

@@ -72,7 +72,8 @@ EXPORTED_SYMBOLS = (
     "gpemu_corr_vector", "gpemu_factorize", "gpemu_solve_lower", "gpemu_solve_upper",
     "gpemu_plan_create", "gpemu_plan_destroy", "gpemu_plan_device_bytes", "gpemu_eval_batch",
     "gpemu_eval_batch_device", "gpemu_plan_last_factor", "gpemu_fit", "gpemu_model_at_theta",
-    "gpemu_model_destroy", "gpemu_predict",
+    "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
+    "gpemu_plan_dag_profile",
 )
 
 
@@ -121,6 +122,9 @@ def lib():
     L.gpemu_eval_batch.argtypes = [_vp, _dp, _sz, _dp, _dp, _dp, _dp, _dp, _ip]
     L.gpemu_eval_batch_device.argtypes = [_vp, _vp, _sz, _vp]
     L.gpemu_plan_last_factor.argtypes = [_vp, _sz, _dp, _dp, _dp]
+    L.gpemu_plan_set_profiling.argtypes = [_vp, C.c_int]
+    L.gpemu_plan_phase_ms.argtypes = [_vp, C.c_int, _dp, _ip]
+    L.gpemu_plan_dag_profile.argtypes = [_vp, C.c_int, C.c_void_p, _sz]
     L.gpemu_fit.argtypes = [_vp, _dp, _dp, C.POINTER(_GaConfigC), C.c_uint64,
                             C.POINTER(_FitResultC), _dp, _dp, _dp, _dp, C.POINTER(_vp)]
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]
@@ -492,6 +496,33 @@ class ProfileEvaluator:
 
     def device_bytes(self) -> int:
         return int(lib().gpemu_plan_device_bytes(self.handle))
+
+    def set_profiling(self, enable: bool):
+        _check(lib().gpemu_plan_set_profiling(self.handle, int(enable)))
+
+    def phase_ms(self, phase: int):
+        """(total device ms, launches) of phase 0 assemble / 1 cholesky / 2 finalize."""
+        t, c = C.c_double(), C.c_int()
+        _check(lib().gpemu_plan_phase_ms(self.handle, phase, C.byref(t), C.byref(c)))
+        return t.value, c.value
+
+    DAG_PHASES = ("ticket", "gemm", "acc_store", "potrf", "diag_store", "border", "off_wait",
+                  "trsm", "off_store", "task_end", "prod_flags", "prod_empty", "n_diag", "n_off",
+                  "slabs", "total")
+
+    def dag_profile(self, enable: bool = True, read: bool = False):
+        """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""
+        out = np.zeros(148 * 16, dtype=np.uint64) if read else None
+        _check(lib().gpemu_plan_dag_profile(self.handle, int(enable),
+                                            None if out is None else out.ctypes.data, 0 if out is None else out.size))
+        if out is None:
+            return None
+        m = out.reshape(-1, 16)
+        return {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
+
+    def eval_batch_device(self, theta_ptr: int, B: int, out_ptr: int):
+        """Device-resident batch: theta_ptr -> B x d doubles, out_ptr -> B x 8 records."""
+        _check(lib().gpemu_eval_batch_device(self.handle, _vp(theta_ptr), B, _vp(out_ptr)))
 
     def eval_batch(self, thetas) -> dict:
         """B independent ProfileEvaluator::eval calls in one device batch."""
