@@ -21,6 +21,12 @@
 extern "C" {
 #endif
 
+#if defined(__GNUC__)
+#define GPEMU_API __attribute__((visibility("default")))
+#else
+#define GPEMU_API
+#endif
+
 /* errors.hpp:9-36 exception hierarchy as status codes */
 typedef enum {
   GPEMU_OK = 0,
@@ -51,70 +57,75 @@ typedef enum {
   GPEMU_ENGINE_SIMPLE = 1  /* one CTA per candidate, unblocked; validation engine */
 } gpemu_engine;
 
-const char* gpemu_last_error(void);
-const char* gpemu_version(void);
+GPEMU_API const char* gpemu_last_error(void);
+GPEMU_API const char* gpemu_version(void);
 
 /* -- context: one device, one stream ------------------------------------ */
-int gpemu_ctx_create(int device, gpemu_ctx** out);
-int gpemu_ctx_destroy(gpemu_ctx* ctx);
+GPEMU_API int gpemu_ctx_create(int device, gpemu_ctx** out);
+GPEMU_API int gpemu_ctx_destroy(gpemu_ctx* ctx);
 /* Use an external cudaStream_t (passed as void*); NULL restores the ctx's own. */
-int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream);
-int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine);
+GPEMU_API int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream);
+GPEMU_API int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine);
 /* Number of kernels this ctx has launched so far (bench accounting). */
-uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx);
+GPEMU_API uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx);
 
 /* -- correlation.hpp ------------------------------------------------------ */
 /* build_corr_matrix (correlation.hpp:99-146) / CorrelationPlan::build_into (:187-223):
  * R (n x n row-major, both triangles written) for one theta. */
-int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
+GPEMU_API int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
                      double p, double nugget, double* R_out);
 /* corr_vector (correlation.hpp:67-91): r_i for one test point, no nugget. */
-int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size_t n, size_t d,
+GPEMU_API int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size_t n, size_t d,
                       const double* theta, double p, double* r_out);
 
 /* -- backend.hpp ---------------------------------------------------------- */
 /* Backend::factorize_into (backend.hpp:102-120): Cholesky of R + jitter I with the
  * kJitterLadder escalation. L_out: n x n row-major, lower triangle meaningful,
  * strict upper zeroed. Returns GPEMU_NOT_PD when the ladder is exhausted. */
-int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
+GPEMU_API int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
                     double* jitter_used);
+/* Backend::try_cholesky (backend.hpp:174, the reference's one virtual compute hook):
+ * ONE in-place attempt on A (n x n row-major, lower triangle read; on success the lower
+ * triangle holds L and the strict upper is zeroed). GPEMU_NOT_PD when a pivot is not
+ * strictly positive (NaN included); A is then unchanged. */
+GPEMU_API int gpemu_try_cholesky(gpemu_ctx* ctx, double* A, size_t n);
 /* Backend::solve_lower_into (:129-140) / solve_upper_into (:143-153). */
-int gpemu_solve_lower(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
-int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
+GPEMU_API int gpemu_solve_lower(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
+GPEMU_API int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const double* b, double* x);
 
 /* -- likelihood.hpp ------------------------------------------------------- */
 /* ProfileEvaluator ctor (likelihood.hpp:77-91): uploads X, y, builds the
  * |dx|^p table on the device. max_batch bounds the candidates per eval call. */
-int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
+GPEMU_API int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
                       double p, double nugget, size_t max_batch, gpemu_plan** out);
-int gpemu_plan_destroy(gpemu_plan* plan);
-size_t gpemu_plan_device_bytes(const gpemu_plan* plan);
+GPEMU_API int gpemu_plan_destroy(gpemu_plan* plan);
+GPEMU_API size_t gpemu_plan_device_bytes(const gpemu_plan* plan);
 
 /* ProfileEvaluator::eval (likelihood.hpp:108-141), batched over B independent
  * thetas (host arrays). Any output pointer may be NULL. Per-slot results are
  * independent of B and of the slot index (batch invariance). */
-int gpemu_eval_batch(gpemu_plan* plan, const double* theta, size_t B, double* neg2, double* mu,
+GPEMU_API int gpemu_eval_batch(gpemu_plan* plan, const double* theta, size_t B, double* neg2, double* mu,
                      double* sigma2, double* jitter, double* log_det, int* slot_status);
 
 /* Same on device memory: d_theta (B x d doubles), d_out (B x 8 doubles:
  * neg2, mu, sigma2, jitter, log_det, status, utu, vtv). Synchronises only to
  * run the jitter ladder (one B-int status read per ladder step). */
-int gpemu_eval_batch_device(gpemu_plan* plan, const double* d_theta, size_t B, double* d_out);
+GPEMU_API int gpemu_eval_batch_device(gpemu_plan* plan, const double* d_theta, size_t B, double* d_out);
 
 /* ProfileEvaluator::last_factor (likelihood.hpp:103) of a batch slot of the most
  * recent eval: L (n x n row-major, strict upper zero). */
-int gpemu_plan_last_factor(gpemu_plan* plan, size_t slot, double* L_out, double* log_det,
+GPEMU_API int gpemu_plan_last_factor(gpemu_plan* plan, size_t slot, double* L_out, double* log_det,
                            double* jitter_used);
 
 /* Per-phase device timing (CUDA events on the plan's stream) for roofline
  * accounting: phase 0 = correlation assembly (K1), 1 = Cholesky engine (K2),
  * 2 = deviance finalisation (K3). Enabling clears previous marks. */
-int gpemu_plan_set_profiling(gpemu_plan* plan, int enable);
-int gpemu_plan_phase_ms(gpemu_plan* plan, int phase, double* total_ms, int* launches);
+GPEMU_API int gpemu_plan_set_profiling(gpemu_plan* plan, int enable);
+GPEMU_API int gpemu_plan_phase_ms(gpemu_plan* plan, int phase, double* total_ms, int* launches);
 /* Diagnostics: per-CTA phase cycle counters of the DAG engine ([num_sms][16], see
  * kernels_chol.cu PR_*). enable=1 (re)arms and zeroes them; out (nullable) receives the
  * counters accumulated since; enable=0 disarms. */
-int gpemu_plan_dag_profile(gpemu_plan* plan, int enable, uint64_t* out, size_t out_len);
+GPEMU_API int gpemu_plan_dag_profile(gpemu_plan* plan, int enable, uint64_t* out, size_t out_len);
 
 /* ---- optimizer.hpp / likelihood.hpp fit ------------------------------- */
 typedef struct {
@@ -136,20 +147,36 @@ typedef struct {
  * (generation, slot) exactly like the sequential reference. theta_hat (d),
  * alpha (n), trace_best (generations), trace_genes (generations*d) may be NULL.
  * model_out (nullable) receives a device-resident GpModel for gpemu_predict. */
-int gpemu_fit(gpemu_plan* plan, const double* lo, const double* hi, const gpemu_ga_config* ga,
+GPEMU_API int gpemu_fit(gpemu_plan* plan, const double* lo, const double* hi, const gpemu_ga_config* ga,
               uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
               double* trace_best, double* trace_genes, gpemu_model** model_out);
 
+/* The reference GA (optimizer.hpp:93-187) as a host-only state machine (no device
+ * needed): gpemu_ga_thetas gives the current generation's P candidates in theta space
+ * (10^genes, likelihood.hpp:265), gpemu_ga_tell takes their -2logL and breeds the next
+ * generation. The candidate sequence is the reference's for any split of a generation
+ * across devices; the status reports the GA incumbent, the fit_gp_detailed stash
+ * (generation, slot) and the GaTrace. gpemu_fit drives the same object. */
+typedef struct gpemu_ga gpemu_ga;
+GPEMU_API int gpemu_ga_create(size_t d, const double* lo, const double* hi, const gpemu_ga_config* cfg,
+                    uint64_t seed, gpemu_ga** out);
+GPEMU_API int gpemu_ga_destroy(gpemu_ga* ga);
+GPEMU_API int gpemu_ga_thetas(const gpemu_ga* ga, double* thetas /* population x d */);
+GPEMU_API int gpemu_ga_tell(gpemu_ga* ga, const double* fitness /* population */);
+GPEMU_API int gpemu_ga_status(const gpemu_ga* ga, int* generation, int* done, double* best_value,
+                    double* best_theta, int* stash_generation, int* stash_slot,
+                    double* trace_best /* generations */, double* trace_genes /* generations x d */);
+
 /* model_at_theta (likelihood.hpp:216-237). scalars: neg2, mu, sigma2, jitter. */
-int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,
+GPEMU_API int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,
                          double* scalars, double* alpha);
-int gpemu_model_destroy(gpemu_model* model);
+GPEMU_API int gpemu_model_destroy(gpemu_model* model);
 
 /* ---- predictor.hpp ------------------------------------------------------ */
 /* predict (predictor.hpp:20-50): yhat_j = mu + r(x_j)' alpha; mse (nullable) is the
  * kriging MSE sigma2 (1 - w'w + (1 - v'w)^2 / v'v), w = L^-1 r, v = L^-1 1
  * (no reference implementation). Validates the unit cube. */
-int gpemu_predict(gpemu_model* model, const double* Xtest, size_t N, double* yhat, double* mse);
+GPEMU_API int gpemu_predict(gpemu_model* model, const double* Xtest, size_t N, double* yhat, double* mse);
 
 #ifdef __cplusplus
 }

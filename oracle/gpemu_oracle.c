@@ -837,67 +837,95 @@ int orc_kriging_mse(const double* X, size_t n, size_t d, const double* theta, do
  * solves, dots and the deviance formula of likelihood.hpp:124-139 all in long
  * double. Used to measure how far the reference itself is from the value it
  * approximates, so parity gates can be conditioning-aware. */
+/* long-double deviance of one (already built, double) R + jitter I */
+static double ld_deviance(const double* R, const double* y, size_t n, double jitter,
+                          long double* L, long double* u, long double* v) {
+  for (size_t i = 0; i < n * n; ++i) L[i] = R[i];
+  for (size_t i = 0; i < n; ++i) L[i * n + i] += jitter;
+  long double logdet = 0.0L;
+  for (size_t j = 0; j < n; ++j) {
+    long double s = L[j * n + j];
+    for (size_t t = 0; t < j; ++t) s -= L[j * n + t] * L[j * n + t];
+    if (!(s > 0.0L)) return INFINITY;
+    const long double dd = sqrtl(s);
+    L[j * n + j] = dd;
+    logdet += logl(dd);
+    for (size_t i = j + 1; i < n; ++i) {
+      long double w = L[i * n + j];
+      for (size_t t = 0; t < j; ++t) w -= L[i * n + t] * L[j * n + t];
+      L[i * n + j] = w / dd;
+    }
+  }
+  for (size_t i = 0; i < n; ++i) {
+    long double su = y[i], sv = 1.0L;
+    for (size_t t = 0; t < i; ++t) {
+      su -= L[i * n + t] * u[t];
+      sv -= L[i * n + t] * v[t];
+    }
+    u[i] = su / L[i * n + i];
+    v[i] = sv / L[i * n + i];
+  }
+  long double utu = 0.0L, vtu = 0.0L, vtv = 0.0L;
+  for (size_t i = 0; i < n; ++i) {
+    utu += u[i] * u[i];
+    vtu += v[i] * u[i];
+    vtv += v[i] * v[i];
+  }
+  const long double mu = vtu / vtv;
+  long double s2 = (utu - 2.0L * mu * vtu + mu * mu * vtv) / (long double)n;
+  if (s2 < 0.0L) s2 = 0.0L;
+  long double qf = (long double)n * s2;
+  if (qf < (long double)DBL_MIN) qf = DBL_MIN;
+  return (double)(2.0L * logdet + (long double)n * logl(qf));
+}
+
 int orc_profile_eval_ld(const double* X, const double* y, size_t n, size_t d, double p,
                         double nugget, const double* thetas, size_t B, const double* jitters,
                         double* neg2_out) {
+  return orc_profile_sensitivity(X, y, n, d, p, nugget, thetas, B, jitters, 0, 0, neg2_out, NULL);
+}
+
+/* Sensitivity of the deviance to 1-ulp relative perturbations of the off-diagonal
+ * entries of R (the accuracy any FP64 R assembly has: exp/log are <= 1 ulp): for each
+ * theta, max over `reps` symmetric random perturbations of |neg2' - neg2| / |neg2|,
+ * all in long double. reps = 0 only fills neg2_out (the truth). */
+int orc_profile_sensitivity(const double* X, const double* y, size_t n, size_t d, double p,
+                            double nugget, const double* thetas, size_t B, const double* jitters,
+                            int reps, uint64_t seed, double* neg2_out, double* sens_out) {
   const size_t pairs = n * (n - 1) / 2;
   double* table = (double*)malloc((pairs * d > 0 ? pairs * d : 1) * sizeof(double));
   double* R = (double*)malloc(n * n * sizeof(double));
+  double* Rp = (double*)malloc(n * n * sizeof(double));
   long double* L = (long double*)malloc(n * n * sizeof(long double));
   long double* u = (long double*)malloc(n * sizeof(long double));
   long double* v = (long double*)malloc(n * sizeof(long double));
-  if (!table || !R || !L || !u || !v) return -2;
+  if (!table || !R || !Rp || !L || !u || !v) return -2;
   orc_corr_table(X, n, d, p, table);
+  orc_rng rng;
+  orc_rng_init(&rng, seed);
   for (size_t b = 0; b < B; ++b) {
     orc_build_from_table(table, n, d, thetas + b * d, nugget, R);
-    int ok = 1;
-    for (size_t i = 0; i < n * n; ++i) L[i] = R[i];
-    for (size_t i = 0; i < n; ++i) L[i * n + i] += jitters[b];
-    long double logdet = 0.0L;
-    for (size_t j = 0; j < n && ok; ++j) {
-      long double s = L[j * n + j];
-      for (size_t t = 0; t < j; ++t) s -= L[j * n + t] * L[j * n + t];
-      if (!(s > 0.0L)) {
-        ok = 0;
-        break;
-      }
-      const long double dd = sqrtl(s);
-      L[j * n + j] = dd;
-      logdet += logl(dd);
-      for (size_t i = j + 1; i < n; ++i) {
-        long double w = L[i * n + j];
-        for (size_t t = 0; t < j; ++t) w -= L[i * n + t] * L[j * n + t];
-        L[i * n + j] = w / dd;
-      }
+    const double t = ld_deviance(R, y, n, jitters[b], L, u, v);
+    neg2_out[b] = t;
+    if (!sens_out) continue;
+    double worst = 0.0;
+    for (int r = 0; r < reps && isfinite(t); ++r) {
+      memcpy(Rp, R, n * n * sizeof(double));
+      for (size_t i = 1; i < n; ++i)
+        for (size_t j = 0; j < i; ++j) {
+          const double e = (2.0 * orc_rng_uniform01(&rng) - 1.0) * 0x1.0p-53;
+          Rp[i * n + j] = R[i * n + j] * (1.0 + e);
+          Rp[j * n + i] = Rp[i * n + j];
+        }
+      const double tp = ld_deviance(Rp, y, n, jitters[b], L, u, v);
+      const double rel = fabs(tp - t) / fabs(t);
+      if (!(rel <= worst)) worst = rel;
     }
-    if (!ok) {
-      neg2_out[b] = INFINITY;
-      continue;
-    }
-    for (size_t i = 0; i < n; ++i) {
-      long double su = y[i], sv = 1.0L;
-      for (size_t t = 0; t < i; ++t) {
-        su -= L[i * n + t] * u[t];
-        sv -= L[i * n + t] * v[t];
-      }
-      u[i] = su / L[i * n + i];
-      v[i] = sv / L[i * n + i];
-    }
-    long double utu = 0.0L, vtu = 0.0L, vtv = 0.0L;
-    for (size_t i = 0; i < n; ++i) {
-      utu += u[i] * u[i];
-      vtu += v[i] * u[i];
-      vtv += v[i] * v[i];
-    }
-    const long double mu = vtu / vtv;
-    long double s2 = (utu - 2.0L * mu * vtu + mu * mu * vtv) / (long double)n;
-    if (s2 < 0.0L) s2 = 0.0L;
-    long double qf = (long double)n * s2;
-    if (qf < (long double)DBL_MIN) qf = DBL_MIN;
-    neg2_out[b] = (double)(2.0L * logdet + (long double)n * logl(qf));
+    sens_out[b] = worst;
   }
   free(table);
   free(R);
+  free(Rp);
   free(L);
   free(u);
   free(v);

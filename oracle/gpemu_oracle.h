@@ -101,6 +101,10 @@ int orc_profile_eval_batch(const double* X, const double* y, size_t n, size_t d,
 int orc_profile_eval_ld(const double* X, const double* y, size_t n, size_t d, double p,
                         double nugget, const double* thetas, size_t B, const double* jitters,
                         double* neg2_out);
+/* ... plus the relative sensitivity of the deviance to 1-ulp perturbations of R. */
+int orc_profile_sensitivity(const double* X, const double* y, size_t n, size_t d, double p,
+                            double nugget, const double* thetas, size_t B, const double* jitters,
+                            int reps, uint64_t seed, double* neg2_out, double* sens_out);
 
 /* ---- optimizer.hpp + likelihood.hpp fit -------------------------------- */
 typedef struct {

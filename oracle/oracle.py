@@ -91,6 +91,8 @@ class Oracle:
         L.orc_kriging_mse.argtypes = [_dp, _sz, _sz, _dp, C.c_double, C.c_double, _dp, _dp, _sz, _dp]
         L.orc_profile_eval_ld.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _sz,
                                           _dp, _dp]
+        L.orc_profile_sensitivity.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp,
+                                              _sz, _dp, C.c_int, _u64, _dp, _dp]
         L.orc_sspe.restype = C.c_double
         L.orc_sspe.argtypes = [_dp, _dp, _sz]
 
@@ -196,6 +198,19 @@ class Oracle:
                                         _ptr(jit), _ptr(out)) != 0:
             raise MemoryError("oracle eval_truth allocation failed")
         return out
+
+    def eval_sensitivity(self, X, y, thetas, p, jitters, nugget=0.0, reps=3, seed=1):
+        """(truth, sensitivity): long-double deviance and its max relative change under
+        `reps` random 1-ulp perturbations of R (conditioning of each candidate)."""
+        X, y, thetas = _f64(X), _f64(y), _f64(np.atleast_2d(thetas))
+        n, d = X.shape
+        B = thetas.shape[0]
+        jit = _f64(np.broadcast_to(jitters, (B,)))
+        truth, sens = np.empty(B), np.empty(B)
+        if self.lib.orc_profile_sensitivity(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
+                                            _ptr(jit), reps, seed, _ptr(truth), _ptr(sens)) != 0:
+            raise MemoryError("oracle eval_sensitivity allocation failed")
+        return truth, sens
 
     def fit(self, X, y, p=1.95, nugget=0.0, lo=1e-6, hi=12.0, population=100, generations=20,
             seed=0, kind=1, want_L=False, crossover_rate=0.9, mutation_sigma=0.15,

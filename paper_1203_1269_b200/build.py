@@ -11,7 +11,7 @@ LIB = os.path.join(HERE, "libgpemu_b200.so")
 SOURCES = ["kernels_corr.cu", "kernels_chol.cu", "kernels_misc.cu", "kernels_predict.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
+         "-Xcompiler", "-fPIC,-fvisibility=hidden", "-Xptxas", "-v", "--expt-relaxed-constexpr"]
 
 
 def _stale() -> bool:

@@ -454,21 +454,34 @@ int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size
   GPEMU_GUARD_END
 }
 
-// Factorization workspace for the Backend-level API (one slot, no table).
-int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
-                    double* jitter_used) {
-  GPEMU_GUARD_BEGIN
-  if (!ctx || !R || n == 0) return set_error(GPEMU_VALIDATION, "factorize: bad argument");
-  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-  gpemu_plan pl;
+// One Cholesky attempt of A (no ladder): Backend::try_cholesky (backend.hpp:174).
+static int factor_once(gpemu_ctx* ctx, gpemu_plan& pl, const double* dR, double jit, int* st,
+                       double* rec) {
+  cudaStream_t s = ctx->stream;
+  ck(cudaMemsetAsync(pl.status.p, 0, sizeof(int), s), "memset");
+  ck(cudaMemsetAsync(pl.borders.p, 0, 2 * pl.Npad * sizeof(double), s), "memset");
+  ck(cudaMemcpyAsync(pl.jitter.p, &jit, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
+  launch_rowmajor_to_tiles(dR, pl.n, pl.NT, jit, pl.factors.p, s);
+  run_chol(&pl, 1);
+  launch_finalize(pl.factors.p, pl.slot_stride, pl.borders.p, pl.status.p, pl.jitter.p, pl.n,
+                  pl.NT, pl.slots.p, 1, pl.out.p, s);
+  ctx->launches += 2;
+  ck(cudaMemcpyAsync(st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+  ck(cudaMemcpyAsync(rec, pl.out.p, REC_SIZE * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+  ck(cudaStreamSynchronize(s), "factorize");
+  int err = 0;
+  ck(cudaMemcpy(&err, pl.error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+  if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
+  return GPEMU_OK;
+}
+
+static void single_slot_plan(gpemu_ctx* ctx, gpemu_plan& pl, size_t n) {
   pl.ctx = ctx;
   pl.n = (int)n;
   pl.NT = (int)((n + TILE - 1) / TILE);
   pl.Npad = pl.NT * TILE;
   pl.slot_stride = (size_t)num_tiles(pl.NT) * TILE_ELEMS;
   cudaStream_t s = ctx->stream;
-  DevBuf<double> dR;
-  dR.alloc(n * n);
   pl.factors.alloc(pl.slot_stride);
   pl.borders.alloc(2 * pl.Npad);
   pl.jitter.alloc(1);
@@ -481,25 +494,49 @@ int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, do
   ck(cudaMemsetAsync(pl.flags.p, 0, pl.flags.count * sizeof(int), s), "memset");
   ck(cudaMemsetAsync(pl.slots.p, 0, sizeof(int), s), "memset");
   ck(cudaMemsetAsync(pl.error.p, 0, sizeof(int), s), "memset");
+}
+
+int gpemu_try_cholesky(gpemu_ctx* ctx, double* A, size_t n) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !A || n == 0) return set_error(GPEMU_VALIDATION, "try_cholesky: bad argument");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  gpemu_plan pl;
+  single_slot_plan(ctx, pl, n);
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dA;
+  dA.alloc(n * n);
+  ck(cudaMemcpyAsync(dA.p, A, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D A");
+  int st = 0;
+  double rec[REC_SIZE];
+  int rc = factor_once(ctx, pl, dA.p, 0.0, &st, rec);
+  if (rc) return rc;
+  if (st != 0) return set_error(GPEMU_NOT_PD, "try_cholesky: pivot not strictly positive");
+  launch_tiles_to_rowmajor(pl.factors.p, pl.n, pl.NT, dA.p, s);
+  ctx->launches += 1;
+  ck(cudaMemcpyAsync(A, dA.p, n * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
+  ck(cudaStreamSynchronize(s), "try_cholesky");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+// Factorization workspace for the Backend-level API (one slot, no table).
+int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, double* log_det,
+                    double* jitter_used) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !R || n == 0) return set_error(GPEMU_VALIDATION, "factorize: bad argument");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  gpemu_plan pl;
+  single_slot_plan(ctx, pl, n);
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dR;
+  dR.alloc(n * n);
   ck(cudaMemcpyAsync(dR.p, R, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D R");
   for (int step = 0; step < 6; ++step) {
     const double jit = kLadder[step];
-    ck(cudaMemsetAsync(pl.status.p, 0, sizeof(int), s), "memset");
-    ck(cudaMemsetAsync(pl.borders.p, 0, 2 * pl.Npad * sizeof(double), s), "memset");
-    ck(cudaMemcpyAsync(pl.jitter.p, &jit, sizeof(double), cudaMemcpyHostToDevice, s), "H2D");
-    launch_rowmajor_to_tiles(dR.p, pl.n, pl.NT, jit, pl.factors.p, s);
-    run_chol(&pl, 1);
-    launch_finalize(pl.factors.p, pl.slot_stride, pl.borders.p, pl.status.p, pl.jitter.p, pl.n,
-                    pl.NT, pl.slots.p, 1, pl.out.p, s);
-    ctx->launches += 2;
     int st = 0;
     double rec[REC_SIZE];
-    ck(cudaMemcpyAsync(&st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
-    ck(cudaMemcpyAsync(rec, pl.out.p, sizeof(rec), cudaMemcpyDeviceToHost, s), "D2H");
-    ck(cudaStreamSynchronize(s), "factorize");
-    int err = 0;
-    ck(cudaMemcpy(&err, pl.error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
-    if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
+    int rc = factor_once(ctx, pl, dR.p, jit, &st, rec);
+    if (rc) return rc;
     if (st == 0) {
       if (L_out) {
         DevBuf<double> dL;
@@ -739,38 +776,28 @@ int gpemu_plan_last_factor(gpemu_plan* pl, size_t slot, double* L_out, double* l
 }
 
 // ---------------------------------------------------------------------------
-int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga_config* gac,
-              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
-              double* trace_best, double* trace_genes, gpemu_model** model_out) {
-  GPEMU_GUARD_BEGIN
-  if (!pl || !lo || !hi || !gac) return set_error(GPEMU_VALIDATION, "fit: null argument");
-  const int d = pl->d;
-  const int P = gac->population, G = gac->generations;
-  // GaConfig::validate (optimizer.hpp:29-38)
-  if (P <= 0 || G <= 0) return set_error(GPEMU_VALIDATION, "GaConfig: population and generations must be positive");
-  if (gac->crossover_rate < 0.0 || gac->crossover_rate > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: crossover_rate must be in [0,1]");
-  if (!(gac->mutation_sigma > 0.0)) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_sigma must be positive");
-  if (gac->mutation_prob < 0.0 || gac->mutation_prob > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_prob must be in [0,1]");
-  if (gac->elitism < 0 || gac->elitism >= P) return set_error(GPEMU_VALIDATION, "GaConfig: elitism must be in [0, population)");
-  if ((size_t)P > pl->max_batch) return set_error(GPEMU_CONFIG, "fit: population %d exceeds the plan's max_batch %zu", P, pl->max_batch);
-  // FitConfig::bounds_for (core.hpp:114-123) + log10 box (likelihood.hpp:247-251)
-  std::vector<double> glo(d), ghi(d);
-  for (int k = 0; k < d; ++k) {
-    if (!(lo[k] > 0.0) || !(lo[k] < hi[k])) return set_error(GPEMU_VALIDATION, "FitConfig: theta bounds require 0 < lower < upper");
-    glo[k] = std::log10(lo[k]);
-    ghi[k] = std::log10(hi[k]);
-    if (!(glo[k] < ghi[k]) || !std::isfinite(glo[k]) || !std::isfinite(ghi[k]))
-      return set_error(GPEMU_VALIDATION, "ga_minimize: degenerate bounds");
-  }
-  const uint64_t ga_seed = derive_seed(seed, 0x9a5eedull);
-  const double mut_prob = gac->mutation_prob > 0.0 ? gac->mutation_prob : 1.0 / (double)d;
-  const int stash = (int)pl->max_batch;  // device slot holding the best factor
-  cudaStream_t s = pl->ctx->stream;
+// ---------------------------------------------------------------------------
+// The reference GA (optimizer.hpp:93-187) as a host state machine: population of the
+// current generation out, its fitness in. Identical candidate sequence to the sequential
+// reference for any evaluation order / batch split; also tracks the fit_gp_detailed stash
+// (likelihood.hpp:257-273: strict <, earliest (generation, slot) wins).
+struct gpemu_ga {
+  int d = 0, P = 0, G = 0, gen = 0;
+  gpemu_ga_config cfg{};
+  uint64_t ga_seed = 0;
+  double mut_prob = 0.0;
+  std::vector<double> glo, ghi;
+  std::vector<std::vector<double>> pop;
+  std::vector<double> fitness;
+  double best_value = INFINITY;  // GA incumbent (record_generation, optimizer.hpp:133-141)
+  std::vector<double> best_point;
+  double stash_value = INFINITY;  // evaluation stash
+  int stash_gen = -1, stash_slot = -1;
+  std::vector<double> trace_best, trace_genes;
 
-  // lhs_population (optimizer.hpp:62-80)
-  Rng init_rng(derive_seed(ga_seed, 0x1e17u));
-  std::vector<std::vector<double>> pop(P, std::vector<double>(d));
-  {
+  void init_population() {
+    Rng init_rng(derive_seed(ga_seed, 0x1e17u));
+    pop.assign(P, std::vector<double>(d));
     std::vector<int> perm(P);
     for (int k = 0; k < d; ++k) {
       std::iota(perm.begin(), perm.end(), 0);
@@ -785,70 +812,22 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
       }
     }
   }
-  std::vector<double> fitness(P), thetas((size_t)P * d);
-  double best_value = INFINITY, stash_value = INFINITY, jitter_max = 0.0;
-  std::vector<double> best_point, stash_theta(d), stash_rec(REC_SIZE, 0.0);
-  std::vector<double> tb(G), tg((size_t)G * d);
 
-  for (int gen = 0; gen < G; ++gen) {
-    if (gen > 0) {
-      std::vector<std::vector<double>> next(P);
-      std::vector<int> order(P);
-      std::iota(order.begin(), order.end(), 0);
-      std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return fitness[a] < fitness[b]; });
-      for (int e = 0; e < gac->elitism; ++e) next[e] = pop[order[e]];
-      for (int slot = gac->elitism; slot < P; ++slot) {
-        Rng rng(derive_seed(ga_seed, (uint64_t)gen, (uint64_t)slot));
-        auto tournament = [&]() -> const std::vector<double>& {
-          const int a = (int)rng.below(P);
-          const int b = (int)rng.below(P);
-          const bool a_wins = fitness[a] < fitness[b] || (fitness[a] == fitness[b] && a <= b);
-          return pop[a_wins ? a : b];
-        };
-        const auto& pa = tournament();
-        const auto& pb = tournament();
-        std::vector<double> child(d);
-        if (rng.uniform01() < gac->crossover_rate) {
-          for (int k = 0; k < d; ++k) child[k] = rng.uniform01() < 0.5 ? pa[k] : pb[k];
-        } else {
-          child = pa;
-        }
-        for (int k = 0; k < d; ++k) {
-          if (rng.uniform01() < mut_prob) child[k] += gac->mutation_sigma * rng.normal();
-          child[k] = std::clamp(child[k], glo[k], ghi[k]);
-        }
-        next[slot] = std::move(child);
-      }
-      pop = std::move(next);
-    }
-    // objective lambda (likelihood.hpp:264-273) over the whole generation
+  void thetas(double* out) const {  // likelihood.hpp:265
     for (int i = 0; i < P; ++i)
-      for (int k = 0; k < d; ++k) thetas[(size_t)i * d + k] = std::pow(10.0, pop[i][k]);
-    ck(cudaMemcpyAsync(pl->theta.p, thetas.data(), thetas.size() * sizeof(double),
-                       cudaMemcpyHostToDevice, s),
-       "H2D theta");
-    int rc = run_batch(pl, P);
-    if (rc) return rc;
-    download_records(pl, P);
+      for (int k = 0; k < d; ++k) out[(size_t)i * d + k] = std::pow(10.0, pop[i][k]);
+  }
+
+  // Records the generation (stash + trace) and breeds the next one.
+  void tell(const double* f) {
+    fitness.assign(f, f + P);
     for (int i = 0; i < P; ++i) {
-      const double* r = &pl->h_out[(size_t)i * REC_SIZE];
-      fitness[i] = r[REC_NEG2];
-      if (pl->last_ladder[i] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[i]]);
-      if (fitness[i] < stash_value) {  // strict <, call order = (generation, slot)
+      if (fitness[i] < stash_value) {
         stash_value = fitness[i];
-        std::copy(r, r + REC_SIZE, stash_rec.begin());
-        std::copy(&thetas[(size_t)i * d], &thetas[(size_t)i * d] + d, stash_theta.begin());
-        ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
-                           pl->factors.p + (size_t)i * pl->slot_stride,
-                           pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
-           "stash factor");
-        ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
-                           pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
-                           cudaMemcpyDeviceToDevice, s),
-           "stash border");
+        stash_gen = gen;
+        stash_slot = i;
       }
     }
-    // record_generation (optimizer.hpp:133-141)
     int b = 0;
     for (int i = 1; i < P; ++i)
       if (fitness[i] < fitness[b]) b = i;
@@ -856,19 +835,175 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
       best_value = fitness[b];
       best_point = pop[b];
     }
-    tb[gen] = fitness[b];
-    std::copy(pop[b].begin(), pop[b].end(), tg.begin() + (size_t)gen * d);
+    trace_best.push_back(fitness[b]);
+    trace_genes.insert(trace_genes.end(), pop[b].begin(), pop[b].end());
+    ++gen;
+    if (gen >= G) return;
+    std::vector<std::vector<double>> next(P);
+    std::vector<int> order(P);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int c) { return fitness[a] < fitness[c]; });
+    for (int e = 0; e < cfg.elitism; ++e) next[e] = pop[order[e]];
+    for (int slot = cfg.elitism; slot < P; ++slot) {
+      Rng rng(derive_seed(ga_seed, (uint64_t)gen, (uint64_t)slot));
+      auto tournament = [&]() -> const std::vector<double>& {
+        const int a = (int)rng.below(P);
+        const int c = (int)rng.below(P);
+        const bool a_wins = fitness[a] < fitness[c] || (fitness[a] == fitness[c] && a <= c);
+        return pop[a_wins ? a : c];
+      };
+      const auto& pa = tournament();
+      const auto& pb = tournament();
+      std::vector<double> child(d);
+      if (rng.uniform01() < cfg.crossover_rate) {
+        for (int k = 0; k < d; ++k) child[k] = rng.uniform01() < 0.5 ? pa[k] : pb[k];
+      } else {
+        child = pa;
+      }
+      for (int k = 0; k < d; ++k) {
+        if (rng.uniform01() < mut_prob) child[k] += cfg.mutation_sigma * rng.normal();
+        child[k] = std::clamp(child[k], glo[k], ghi[k]);
+      }
+      next[slot] = std::move(child);
+    }
+    pop = std::move(next);
+  }
+};
+
+static int ga_setup(gpemu_ga* g, size_t d, const double* lo, const double* hi,
+                    const gpemu_ga_config* gac, uint64_t seed) {
+  const int P = gac->population, G = gac->generations;
+  // GaConfig::validate (optimizer.hpp:29-38)
+  if (P <= 0 || G <= 0) return set_error(GPEMU_VALIDATION, "GaConfig: population and generations must be positive");
+  if (gac->crossover_rate < 0.0 || gac->crossover_rate > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: crossover_rate must be in [0,1]");
+  if (!(gac->mutation_sigma > 0.0)) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_sigma must be positive");
+  if (gac->mutation_prob < 0.0 || gac->mutation_prob > 1.0) return set_error(GPEMU_VALIDATION, "GaConfig: mutation_prob must be in [0,1]");
+  if (gac->elitism < 0 || gac->elitism >= P) return set_error(GPEMU_VALIDATION, "GaConfig: elitism must be in [0, population)");
+  if (d == 0) return set_error(GPEMU_VALIDATION, "ga_minimize: empty bounds");
+  g->d = (int)d;
+  g->P = P;
+  g->G = G;
+  g->cfg = *gac;
+  g->glo.resize(d);
+  g->ghi.resize(d);
+  // FitConfig::bounds_for (core.hpp:114-123) + log10 box (likelihood.hpp:247-251)
+  for (size_t k = 0; k < d; ++k) {
+    if (!(lo[k] > 0.0) || !(lo[k] < hi[k])) return set_error(GPEMU_VALIDATION, "FitConfig: theta bounds require 0 < lower < upper");
+    g->glo[k] = std::log10(lo[k]);
+    g->ghi[k] = std::log10(hi[k]);
+    if (!(g->glo[k] < g->ghi[k]) || !std::isfinite(g->glo[k]) || !std::isfinite(g->ghi[k]))
+      return set_error(GPEMU_VALIDATION, "ga_minimize: degenerate bounds");
+  }
+  g->ga_seed = derive_seed(seed, 0x9a5eedull);  // likelihood.hpp:276
+  g->mut_prob = gac->mutation_prob > 0.0 ? gac->mutation_prob : 1.0 / (double)d;
+  g->init_population();
+  return GPEMU_OK;
+}
+
+int gpemu_ga_create(size_t d, const double* lo, const double* hi, const gpemu_ga_config* cfg,
+                    uint64_t seed, gpemu_ga** out) {
+  if (!lo || !hi || !cfg || !out) return set_error(GPEMU_VALIDATION, "ga_create: null argument");
+  auto* g = new gpemu_ga();
+  int rc = ga_setup(g, d, lo, hi, cfg, seed);
+  if (rc) {
+    delete g;
+    return rc;
+  }
+  *out = g;
+  return GPEMU_OK;
+}
+
+int gpemu_ga_destroy(gpemu_ga* g) {
+  delete g;
+  return GPEMU_OK;
+}
+
+int gpemu_ga_thetas(const gpemu_ga* g, double* thetas) {
+  if (!g || !thetas) return set_error(GPEMU_VALIDATION, "ga_thetas: null argument");
+  if (g->gen >= g->G) return set_error(GPEMU_VALIDATION, "ga_thetas: the GA is finished");
+  g->thetas(thetas);
+  return GPEMU_OK;
+}
+
+int gpemu_ga_tell(gpemu_ga* g, const double* fitness) {
+  if (!g || !fitness) return set_error(GPEMU_VALIDATION, "ga_tell: null argument");
+  if (g->gen >= g->G) return set_error(GPEMU_VALIDATION, "ga_tell: the GA is finished");
+  g->tell(fitness);
+  return GPEMU_OK;
+}
+
+int gpemu_ga_status(const gpemu_ga* g, int* generation, int* done, double* best_value,
+                    double* best_theta, int* stash_generation, int* stash_slot,
+                    double* trace_best, double* trace_genes) {
+  if (!g) return set_error(GPEMU_VALIDATION, "ga_status: null argument");
+  if (generation) *generation = g->gen;
+  if (done) *done = g->gen >= g->G;
+  if (best_value) *best_value = g->best_value;
+  if (best_theta && !g->best_point.empty())
+    for (int k = 0; k < g->d; ++k) best_theta[k] = std::pow(10.0, g->best_point[k]);
+  if (stash_generation) *stash_generation = g->stash_gen;
+  if (stash_slot) *stash_slot = g->stash_slot;
+  if (trace_best) std::copy(g->trace_best.begin(), g->trace_best.end(), trace_best);
+  if (trace_genes) std::copy(g->trace_genes.begin(), g->trace_genes.end(), trace_genes);
+  return GPEMU_OK;
+}
+
+int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga_config* gac,
+              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
+              double* trace_best, double* trace_genes, gpemu_model** model_out) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !lo || !hi || !gac) return set_error(GPEMU_VALIDATION, "fit: null argument");
+  gpemu_ga ga;
+  int rc = ga_setup(&ga, pl->d, lo, hi, gac, seed);
+  if (rc) return rc;
+  const int d = pl->d, P = ga.P;
+  if ((size_t)P > pl->max_batch)
+    return set_error(GPEMU_CONFIG, "fit: population %d exceeds the plan's max_batch %zu", P, pl->max_batch);
+  const int stash = (int)pl->max_batch;  // device slot holding the best factor
+  cudaStream_t s = pl->ctx->stream;
+  std::vector<double> thetas((size_t)P * d), fitness(P), stash_theta(d), stash_rec(REC_SIZE, 0.0);
+  double jitter_max = 0.0;
+  while (ga.gen < ga.G) {
+    // objective lambda (likelihood.hpp:264-273) over the whole generation: one batch
+    ga.thetas(thetas.data());
+    ck(cudaMemcpyAsync(pl->theta.p, thetas.data(), thetas.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, s),
+       "H2D theta");
+    rc = run_batch(pl, P);
+    if (rc) return rc;
+    download_records(pl, P);
+    const double prev_stash = ga.stash_value;
+    for (int i = 0; i < P; ++i) {
+      fitness[i] = pl->h_out[(size_t)i * REC_SIZE + REC_NEG2];
+      if (pl->last_ladder[i] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[i]]);
+    }
+    const int gen_now = ga.gen;
+    ga.tell(fitness.data());
+    if (ga.stash_value < prev_stash && ga.stash_gen == gen_now) {
+      const int i = ga.stash_slot;  // keep the best factor on the device (likelihood.hpp:270)
+      const double* r = &pl->h_out[(size_t)i * REC_SIZE];
+      std::copy(r, r + REC_SIZE, stash_rec.begin());
+      std::copy(&thetas[(size_t)i * d], &thetas[(size_t)i * d] + d, stash_theta.begin());
+      ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
+                         pl->factors.p + (size_t)i * pl->slot_stride,
+                         pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
+         "stash factor");
+      ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
+                         pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
+                         cudaMemcpyDeviceToDevice, s),
+         "stash border");
+    }
   }
   ck(cudaStreamSynchronize(s), "fit");
-  if (!std::isfinite(stash_value))
+  if (!std::isfinite(ga.stash_value))
     return set_error(GPEMU_FIT, "fit_gp: every candidate failed factorization (n = %d)", pl->n);
-  if (best_value != stash_value)
+  if (ga.best_value != ga.stash_value)
     return set_error(GPEMU_ERROR, "fit_gp: optimizer incumbent diverged from evaluation stash");
   gpemu_model* m = make_model(pl, stash, stash_theta.data(), stash_rec.data());
   if (theta_hat) std::copy(stash_theta.begin(), stash_theta.end(), theta_hat);
   if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
-  if (trace_best) std::copy(tb.begin(), tb.end(), trace_best);
-  if (trace_genes) std::copy(tg.begin(), tg.end(), trace_genes);
+  if (trace_best) std::copy(ga.trace_best.begin(), ga.trace_best.end(), trace_best);
+  if (trace_genes) std::copy(ga.trace_genes.begin(), ga.trace_genes.end(), trace_genes);
   if (res) {
     res->neg2_log_lik = stash_rec[REC_NEG2];
     res->mu_hat = stash_rec[REC_MU];

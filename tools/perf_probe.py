@@ -6,11 +6,13 @@ sys.path.insert(0, "/root/repo")
 import paper_1203_1269_b200.gpemu as g
 
 n, d, B = (int(a) for a in (sys.argv[1:4] if len(sys.argv) > 3 else (4096, 10, 100)))
+p_exp = float(sys.argv[4]) if len(sys.argv) > 4 else 1.95
+nug = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
 rng = np.random.default_rng(0)
 X = rng.random((n, d))
 y = np.sin(3 * X).sum(1)
 ctx = g.Context(0, "dag")
-ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=B)
+ev = g.ProfileEvaluator(g.new_dataset(X, y), p_exp, nug, g.Backend(ctx), max_batch=B)
 th = 10 ** rng.uniform(-1.0, 0.5, size=(B, d))
 dth = torch.from_numpy(th).cuda()
 out = torch.empty(B * 8, dtype=torch.float64, device="cuda")
