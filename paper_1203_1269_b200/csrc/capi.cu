@@ -184,7 +184,11 @@ struct gpemu_model {
   int n = 0, d = 0, NT = 0;
   double p = 1.95, mu = 0.0, sigma2 = 0.0, vtv = 0.0, neg2 = 0.0, jitter = 0.0;
   std::vector<double> theta;
-  DevBuf<double> X, theta_d, alpha, tiles, v;
+  DevBuf<double> X, theta_d, alpha, tiles, u, v;
+  // extension-mode workspace for the MSE (test-point row tiles)
+  DevBuf<double> ext;
+  DevBuf<int> ext_flags, ext_slot, counter, error;
+  int ext_rt_cap = 0, epoch = 0;
 };
 
 namespace {
@@ -319,12 +323,16 @@ gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const dou
   m->theta_d.alloc(pl->d);
   m->alpha.alloc(pl->n);
   m->tiles.alloc(pl->slot_stride);
+  m->u.alloc(pl->Npad);
   m->v.alloc(pl->Npad);
   ck(cudaMemcpyAsync(m->X.p, pl->X.p, (size_t)pl->n * pl->d * sizeof(double), cudaMemcpyDeviceToDevice, s), "model X");
   ck(cudaMemcpyAsync(m->theta_d.p, theta, pl->d * sizeof(double), cudaMemcpyHostToDevice, s), "model theta");
   ck(cudaMemcpyAsync(m->tiles.p, pl->factors.p + (size_t)slot * pl->slot_stride,
                      pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
      "model tiles");
+  ck(cudaMemcpyAsync(m->u.p, pl->borders.p + (size_t)slot * 2 * pl->Npad,
+                     pl->Npad * sizeof(double), cudaMemcpyDeviceToDevice, s),
+     "model u");
   ck(cudaMemcpyAsync(m->v.p, pl->borders.p + (size_t)slot * 2 * pl->Npad + pl->Npad,
                      pl->Npad * sizeof(double), cudaMemcpyDeviceToDevice, s),
      "model v");
@@ -1075,10 +1083,50 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
                  bad.p, s);
   m->ctx->launches += 1;
   if (mse) {
+    // W = L^-1 r for chunks of test points as extension rows of the factor (DMMA tiles),
+    // then one warp per point: the kriging MSE (and yhat from w, which is not used here:
+    // yhat keeps the reference's r.alpha route above).
     dm.alloc(N);
-    launch_predict_mse(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->sigma2,
-                       m->tiles.p, m->NT, m->v.p, m->vtv, nullptr, dm.p, bad.p, s);
-    m->ctx->launches += 1;
+    const int NT = m->NT;
+    const int chunk_pts = 65536;
+    const int rt_cap = (int)std::min<size_t>((N + TILE - 1) / TILE, chunk_pts / TILE);
+    if (m->ext_rt_cap < rt_cap) {
+      m->ext.alloc((size_t)rt_cap * NT * TILE_ELEMS);
+      m->ext_flags.alloc((size_t)rt_cap * NT);
+      ck(cudaMemset(m->ext_flags.p, 0, (size_t)rt_cap * NT * sizeof(int)), "memset");
+      m->ext_slot.alloc(1);
+      ck(cudaMemset(m->ext_slot.p, 0, sizeof(int)), "memset");
+      m->counter.alloc(1);
+      m->error.alloc(1);
+      ck(cudaMemset(m->error.p, 0, sizeof(int)), "memset");
+      m->ext_rt_cap = rt_cap;
+    }
+    for (size_t p0 = 0; p0 < N; p0 += chunk_pts) {
+      const int Nc = (int)std::min<size_t>(chunk_pts, N - p0);
+      const int RT = (Nc + TILE - 1) / TILE;
+      launch_cross_tiles(dXt.p + p0 * m->d, Nc, m->X.p, m->n, m->d, m->theta_d.p, m->p, NT, RT,
+                         m->ext.p, bad.p, s);
+      DagLaunch a;
+      a.factors = m->tiles.p;
+      a.borders = nullptr;
+      a.slot_stride = 0;
+      a.n = m->n;
+      a.NT = NT;
+      a.slots = m->ext_slot.p;
+      a.nslots = 1;
+      a.counter = m->counter.p;
+      a.flags = nullptr;
+      a.epoch = ++m->epoch;
+      a.status = nullptr;
+      a.error = m->error.p;
+      a.ext = m->ext.p;
+      a.ext_rt = RT;
+      a.ext_flags = m->ext_flags.p;
+      launch_chol_dag(a, m->ctx->num_sms, s);
+      launch_ext_reduce(m->ext.p, Nc, m->n, NT, m->u.p, m->v.p, m->mu, m->sigma2, m->vtv,
+                        nullptr, dm.p + p0, s);
+      m->ctx->launches += 3;
+    }
   }
   ck(cudaGetLastError(), "predict launch");
   int hbad = 0;
@@ -1086,6 +1134,11 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   if (mse) ck(cudaMemcpyAsync(mse, dm.p, N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H mse");
   ck(cudaMemcpyAsync(&hbad, bad.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H bad");
   ck(cudaStreamSynchronize(s), "predict");
+  if (mse && m->error.p) {
+    int err = 0;
+    ck(cudaMemcpy(&err, m->error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H error");
+    if (err) return set_error(GPEMU_CUDA, "chol_dag (extension): dependency wait timed out");
+  }
   if (hbad) return set_error(GPEMU_NONFINITE, "corr_vector: non-finite correlation value");
   return GPEMU_OK;
   GPEMU_GUARD_END

@@ -40,6 +40,10 @@ struct DagLaunch {
   int* status;     // [slot]
   int* error;      // deadlock / timeout word
   unsigned long long* prof = nullptr;  // optional [grid][16] phase cycle counters
+  // extension mode (prediction MSE): ext_rt row tiles of test points, [It][NT] tiles
+  double* ext = nullptr;
+  int ext_rt = 0;
+  int* ext_flags = nullptr;  // [It][NT]
 };
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s);
 void launch_chol_simple(const DagLaunch& a, cudaStream_t s);
@@ -72,5 +76,15 @@ void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
                         const double* theta, double p, double sigma2, const double* tiles, int NT,
                         const double* v /* L^-1 1 */, double vtv, double* work /*N*Npad*/,
                         double* mse, int* bad, cudaStream_t s);
+// Cross-correlation tiles of RT*128 test points against the design, [It][J] tile layout
+// (rows past N and columns past n are zero).
+void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,
+                        const double* theta, double p, int NT, int RT, double* ext, int* bad,
+                        cudaStream_t s);
+// Per test point from W = L^-1 r (ext tiles): yhat = mu + w.(u - mu v), mse =
+// sigma2 (1 - w'w + (1 - v'w)^2 / v'v).
+void launch_ext_reduce(const double* ext, int N, int n, int NT, const double* u, const double* v,
+                       double mu, double sigma2, double vtv, double* yhat, double* mse,
+                       cudaStream_t s);
 
 }  // namespace gpemu_dev

@@ -287,7 +287,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   const int warp = tid >> 5, lane = tid & 31;
   const int NT = a.NT, B = a.nslots, n = a.n;
   const int Npad = NT * TILE;
-  const int ntasks = B * NT * (NT + 1) / 2;
+  // Extension mode (a.ext != null): rows of test points appended below the factor; only
+  // OFF tasks W(It, j) = (Rt(It, j) - sum_K W(It, K) L(j, K)^T) L(j, j)^-T, ordered
+  // column-major; the factor tiles are final, only the row's own earlier tiles are waited on.
+  const bool ext = a.ext != nullptr;
+  const int ntasks = ext ? a.ext_rt * NT : B * NT * (NT + 1) / 2;
   const int epoch = a.epoch;
   const size_t fstride = (size_t)(NT + 1) * NT;
 
@@ -310,10 +314,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     if (tid == 0) {
       const int t = atomicAdd(a.counter, 1);
       misc->ticket = t;
-      if (t < ntasks) {
+      if (t < ntasks && !ext) {
         int bpos, j, I;
         decode_task(t, B, NT, bpos, j, I);
         misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
+      } else {
+        misc->skip = 0;
       }
       misc->fail = 0;
     }
@@ -321,8 +327,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     const int t = misc->ticket;
     if (t >= ntasks) break;
     if (tid == 0) pr.lap(PR_TICKET);
-    int bpos, j, I;
-    decode_task(t, B, NT, bpos, j, I);
+    int bpos, j, I, It = 0;
+    if (ext) {
+      j = t / a.ext_rt;
+      It = t - j * a.ext_rt;
+      I = NT;  // below every factor row: never a DIAG task
+      bpos = 0;
+    } else {
+      decode_task(t, B, NT, bpos, j, I);
+    }
     const bool diag = (I == j);
     const int slot = a.slots[bpos];
     const bool skip = misc->skip != 0;
@@ -338,7 +351,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // row of the result stays in one warp, so the OFF-task TRSM needs no block barrier.
       const int lr = lane >> 2, lc = lane & 3;
       const int brow = tid >> 7, bc = tid & 127;  // border accumulation role (DIAG)
-      double* gtile = fac + tile_index(I, j) * TILE_ELEMS;
+      // tile (row I, col K): the factor's packed lower tiles, or the extension rows
+      auto a_tile = [&](int K) -> double* {
+        return ext ? a.ext + ((size_t)It * NT + K) * TILE_ELEMS : fac + tile_index(I, K) * TILE_ELEMS;
+      };
+      double* gtile = a_tile(j);
       // Accumulators start from R(I,j) and the products are SUBTRACTED (negated A
       // operand, free in DMMA): the running-residual order of the reference's
       // `v -= L_it * L_jt` (backend.hpp:197-204), which keeps the rounding error
@@ -362,11 +379,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         const int K = p >> 2, sq = p & 3;
         if (sq == 0) {
           pr.start();
-          wait_flag(&flags[j * NT + K], epoch, a.error);
-          if (diag) {
-            wait_flag(&flags[NT * NT + K], epoch, a.error);
+          if (ext) {
+            wait_flag(&a.ext_flags[(size_t)It * NT + K], epoch, a.error);
           } else {
-            wait_flag(&flags[I * NT + K], epoch, a.error);
+            wait_flag(&flags[j * NT + K], epoch, a.error);
+            if (diag) {
+              wait_flag(&flags[NT * NT + K], epoch, a.error);
+            } else {
+              wait_flag(&flags[I * NT + K], epoch, a.error);
+            }
           }
           fence_proxy_async_global();
           pr.lap(PR_PROD_FLAGS);
@@ -378,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         pr.lap(PR_PROD_EMPTY);
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
         mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
-        bulk_g2s(dst, fac + tile_index(I, K) * TILE_ELEMS + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
+        bulk_g2s(dst, a_tile(K) + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
         if (!diag)
           bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
                    kSlabBytes, &full[stage]);
@@ -514,7 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // the right, (c) store the finished block, (d) rotate the accumulator window.
         if (!skip) {
           if (tid == 0) {
-            wait_flag(&flags[j * NT + j], epoch, a.error);
+            if (!ext) wait_flag(&flags[j * NT + j], epoch, a.error);
             fence_proxy_async_global();
             mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
             const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
@@ -526,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           ++ljj_phase;
         }
         if (tid == 0) pr.lap(PR_OFF_WAIT);
-        const bool run = !skip && *((volatile int*)&a.status[slot]) == 0;
+        const bool run = !skip && (ext || *((volatile int*)&a.status[slot]) == 0);
         if (run) {
           const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
           // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
@@ -607,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
         consumer_sync();
         if (tid == 0) {
-          publish_flag(&flags[I * NT + j], epoch);
+          publish_flag(ext ? &a.ext_flags[(size_t)It * NT + j] : &flags[I * NT + j], epoch);
           pr.lap(PR_OFF_STORE);
         }
       }
@@ -627,7 +648,7 @@ void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s) {
     cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     configured = true;
   }
-  const int ntasks = a.nslots * a.NT * (a.NT + 1) / 2;
+  const int ntasks = a.ext ? a.ext_rt * a.NT : a.nslots * a.NT * (a.NT + 1) / 2;
   const int grid = ntasks < num_sms ? ntasks : num_sms;
   cudaMemsetAsync(a.counter, 0, sizeof(int), s);
   chol_dag_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);

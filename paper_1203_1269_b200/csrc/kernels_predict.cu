@@ -180,3 +180,107 @@ void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
 }
 
 }  // namespace gpemu_dev
+
+namespace gpemu_dev {
+
+// ---------------------------------------------------------------------------
+// MSE at scale: test points become extra row tiles below the factor. The DAG engine in
+// extension mode turns each row of cross-correlations r into w = L^-1 r with DMMA tiles
+// (the same OFF-task path as the factorization), then one warp per point reduces its row.
+
+// Cross-correlation tile (It, J): rows = test points It*128 + r, cols = design points
+// J*128 + c; corr_vector arithmetic (correlation.hpp:84-87): sequential k, no FMA.
+__global__ void __launch_bounds__(256) cross_tiles_kernel(const double* __restrict__ Xt, int N,
+                                                          const double* __restrict__ X, int n,
+                                                          int d, const double* __restrict__ theta,
+                                                          double p, int NT,
+                                                          double* __restrict__ ext, int* bad) {
+  extern __shared__ double sm[];
+  double* xt = sm;                 // [128][d]
+  double* xs = xt + TILE * d;      // [128][d]
+  double* th = xs + TILE * d;      // [d]
+  const int tile = blockIdx.x;
+  const int It = tile / NT, J = tile - It * NT;
+  for (int q = threadIdx.x; q < TILE * d; q += blockDim.x) {
+    const int r = q / d, k = q - r * d;
+    const int pt = It * TILE + r, pi = J * TILE + r;
+    xt[q] = pt < N ? Xt[(size_t)pt * d + k] : 0.0;
+    xs[q] = pi < n ? X[(size_t)pi * d + k] : 0.0;
+  }
+  for (int k = threadIdx.x; k < d; k += blockDim.x) th[k] = theta[k];
+  __syncthreads();
+  double* out = ext + (size_t)tile * TILE_ELEMS;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    int r, c;
+    elem_rc(e, r, c);
+    double v = 0.0;
+    if (It * TILE + r < N && J * TILE + c < n) {
+      double s = 0.0;
+      for (int k = 0; k < d; ++k)
+        s = __dadd_rn(s, __dmul_rn(th[k], pow_abs_p(xt[r * d + k] - xs[c * d + k], p)));
+      v = exp(-s);
+      if (!isfinite(v)) *bad = 1;
+    }
+    out[e] = v;
+  }
+}
+
+void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,
+                        const double* theta, double p, int NT, int RT, double* ext, int* bad,
+                        cudaStream_t s) {
+  const size_t smem = (2 * (size_t)TILE * d + d) * sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(cross_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cross_tiles_kernel<<<dim3(RT * NT, 4), 256, smem, s>>>(Xt, N, X, n, d, theta, p, NT, ext, bad);
+}
+
+// One warp per test point: fixed-order lane partials + shuffle tree (deterministic).
+__global__ void __launch_bounds__(256) ext_reduce_kernel(const double* __restrict__ ext, int N,
+                                                         int n, int NT,
+                                                         const double* __restrict__ u,
+                                                         const double* __restrict__ v, double mu,
+                                                         double sigma2, double vtv,
+                                                         double* __restrict__ yhat,
+                                                         double* __restrict__ mse) {
+  const int lane = threadIdx.x & 31;
+  const int pt = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (pt >= N) return;
+  const int It = pt >> 7, r = pt & 127;
+  double ww = 0.0, vw = 0.0, yw = 0.0;
+  for (int J = 0; J < NT; ++J) {
+    const double* tl = ext + ((size_t)It * NT + J) * TILE_ELEMS;
+#pragma unroll
+    for (int sl = 0; sl < SLABS_PER_TILE; ++sl) {
+      const int c = sl * SLAB + lane;
+      const int col = J * TILE + c;
+      if (col < n) {
+        const double w = tl[elem_off(r, c)];
+        ww = fma(w, w, ww);
+        vw = fma(v[col], w, vw);
+        yw = fma(u[col] - mu * v[col], w, yw);
+      }
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    ww += __shfl_xor_sync(0xffffffffu, ww, off);
+    vw += __shfl_xor_sync(0xffffffffu, vw, off);
+    yw += __shfl_xor_sync(0xffffffffu, yw, off);
+  }
+  if (lane == 0) {
+    if (yhat) yhat[pt] = mu + yw;
+    if (mse) {
+      const double a = 1.0 - vw;
+      const double s2 = sigma2 * (1.0 - ww + a * a / vtv);
+      mse[pt] = s2 < 0.0 ? 0.0 : s2;
+    }
+  }
+}
+
+void launch_ext_reduce(const double* ext, int N, int n, int NT, const double* u, const double* v,
+                       double mu, double sigma2, double vtv, double* yhat, double* mse,
+                       cudaStream_t s) {
+  ext_reduce_kernel<<<(N + 7) / 8, 256, 0, s>>>(ext, N, n, NT, u, v, mu, sigma2, vtv, yhat, mse);
+}
+
+}  // namespace gpemu_dev

@@ -274,3 +274,22 @@ def test_predict_and_mse_vs_oracle(g, ctx, orc):
     assert np.all(mt <= 1e-8 * mp["sigma2"][0])
     with pytest.raises(g.ValidationError):
         g.predict(m, np.array([[0.5, 1.5]]))
+
+
+def test_mse_extension_rows_multi_tile(g, ctx, orc):
+    """MSE through the DAG extension mode across several tile rows/cols (n=700, N=300)."""
+    rng = np.random.default_rng(77)
+    n, d = 700, 3
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1) + 0.5 * (X * X).sum(1)
+    th = np.array([4.0, 2.5, 6.0])
+    m = g.model_at_theta(g.new_dataset(X, y), th, 1.95, 0.0, g.Backend(ctx))
+    ref = orc.eval_batch(X, y, th[None, :], 1.95)
+    L, ld, jt = orc.factorize(orc.build_corr(X, th, 1.95))
+    Xt = rng.random((300, d))
+    yhat, mse = g.predict(m, Xt, with_mse=True)
+    mo = orc.kriging_mse(X, th, 1.95, ref["sigma2"][0], L, Xt)
+    assert np.max(np.abs(mse - mo)) <= 1e-7 * ref["sigma2"][0]
+    alpha = orc.solve_upper(L, orc.solve_lower(L, y - ref["mu"][0]))
+    yo = orc.predict(X, th, 1.95, ref["mu"][0], alpha, Xt)
+    assert np.max(np.abs(yhat - yo)) <= 1e-8 * max(np.abs(yo).max(), np.abs(y).max())
