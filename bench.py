@@ -149,7 +149,7 @@ def run_reference_arm(args, rank, world):
         return {"impl": "reference", "unavailable": "oracle/_ref/libgpemu_ref_fast.so not built"}
     ref = RefLib(fast=True)
     X, y, batches = make_inputs(args, 0)
-    per_step = args.cpu_sample or 2
+    per_step = args.cpu_sample or 4
     th = batches[0]
     ref.eval_batch_timed(X, y, th[:1], args.p)  # page-in; the plan is excluded from timing below
     evals, secs, plan_s = 0, 0.0, 0.0
