@@ -125,6 +125,7 @@ constexpr int kOffW = kOffBar + 256;                    // border w: 2 x 128 dou
 constexpr int kOffMisc = kOffW + 2 * TILE * 8;          // task scalars
 constexpr int kSmemBytes = kOffMisc + 64;
 constexpr long long kSpinLimitCycles = 20000000000LL;  // ~10 s: declare deadlock
+constexpr int kStageLd = 18;  // row stride (doubles) of the per-warp TRSM staging block
 
 struct Misc {
   int ticket;
@@ -551,37 +552,64 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (run) {
           const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
           // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
-          // a*r + one FMA correction (division rounding as in backend.hpp:206)
+          // a*r + one FMA correction (division rounding as in backend.hpp:206).
+          // The eight diagonal 16x16 blocks of L(j,j) are copied densely so the in-block
+          // substitution reads them as warp-uniform (broadcast) loads with immediate offsets.
           double* rinv = W;
+          double* Dd = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);       // [8][16][16]
+          double* St = reinterpret_cast<double*>(smem + TILE_ELEMS * 8 + 2048 * 8) +
+                       warp * (16 * kStageLd);                                   // [16][kStageLd]
           if (tid < TILE) rinv[tid] = 1.0 / Ls[elem_off(tid, tid)];
+          for (int q = tid; q < 2048; q += kConsumers) {
+            const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
+            Dd[q] = cc <= rr ? Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)] : 0.0;
+          }
           consumer_sync();
           const int qbase = lane & ~3;
           for (int cb = 0; cb < 8; ++cb) {
             const int o = 16 * cb;
-            // (a) columns o..o+15 live in acc[mi][0..1] (rotated window)
+            // (a) columns o..o+15 (acc[mi][0..1], rotated window): through the warp's
+            // staging block so lane r < 16 owns row r and substitutes in registers
 #pragma unroll
-            for (int c = 0; c < 16; ++c) {
-              const int nsub = c >> 3, q = (c & 7) >> 1, e = c & 1;
-              const double rcc = rinv[o + c];
-              const double lcc = Ls[elem_off(o + c, o + c)];
+            for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-              for (int mi = 0; mi < 2; ++mi) {
-                // quotient a / L_cc: reciprocal estimate + one FMA residual correction
-                // (the rounding of a true division, without the DDIV call sequence)
-                const double av0 = acc[mi][nsub][e];
-                const double x0 = av0 * rcc;
-                double x = fma(fma(-x0, lcc, av0), rcc, x0);
-                x = __shfl_sync(0xffffffffu, x, qbase | q);
-                if (lc == q) acc[mi][nsub][e] = x;
+              for (int nsub = 0; nsub < 2; ++nsub)
+                *reinterpret_cast<double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc) =
+                    make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+            __syncwarp();
+            if (lane < 16) {
+              double xr[16];
+              double* row = St + lane * kStageLd;
 #pragma unroll
-                for (int ns2 = 0; ns2 < 2; ++ns2)
-#pragma unroll
-                  for (int e2 = 0; e2 < 2; ++e2) {
-                    const int c2 = 8 * ns2 + 2 * lc + e2;
-                    if (c2 > c) acc[mi][ns2][e2] -= x * Ls[elem_off(o + c2, o + c)];
-                  }
+              for (int c = 0; c < 16; c += 2) {
+                const double2 v = *reinterpret_cast<const double2*>(row + c);
+                xr[c] = v.x;
+                xr[c + 1] = v.y;
               }
+              const double* D = Dd + cb * 256;
+              const double* ri = rinv + o;
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const double rcc = ri[c], lcc = D[c * 16 + c];
+                const double x0 = xr[c] * rcc;
+                xr[c] = fma(fma(-x0, lcc, xr[c]), rcc, x0);
+#pragma unroll
+                for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] -= xr[c] * D[c2 * 16 + c];
+              }
+#pragma unroll
+              for (int c = 0; c < 16; c += 2)
+                *reinterpret_cast<double2*>(row + c) = make_double2(xr[c], xr[c + 1]);
             }
+            __syncwarp();
+#pragma unroll
+            for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+              for (int nsub = 0; nsub < 2; ++nsub) {
+                const double2 v =
+                    *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc);
+                acc[mi][nsub][0] = v.x;
+                acc[mi][nsub][1] = v.y;
+              }
             // (b) acc[:, 2..] -= X_block * L(j,j)[rows right of the block, block cols]^T
             if (cb < 7) {
               double av[2][4];
