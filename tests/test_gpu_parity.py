@@ -293,3 +293,19 @@ def test_mse_extension_rows_multi_tile(g, ctx, orc):
     alpha = orc.solve_upper(L, orc.solve_lower(L, y - ref["mu"][0]))
     yo = orc.predict(X, th, 1.95, ref["mu"][0], alpha, Xt)
     assert np.max(np.abs(yhat - yo)) <= 1e-8 * max(np.abs(yo).max(), np.abs(y).max())
+
+
+@pytest.mark.parametrize("engine", ["simple", "dag"])
+@pytest.mark.parametrize("name", ["x_d20_nugget", "x_p1", "x_d1"])
+def test_eval_batch_extra_shapes(g, name, engine):
+    """d=20 with a nugget (C4-like), the exponential kernel p=1, and d=1 (nugget 0.01)."""
+    z = np.load(os.path.join(GOLD, f"{name}.npz"))
+    be = g.Backend(g.Context(0, engine))
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), float(z["p"]), float(z["nugget"]), be,
+                            max_batch=16)
+    r = ev.eval_batch(z["thetas"])
+    assert np.array_equal(r["jitter"], z["jitter"])
+    gate_neg2(r["neg2"], z)
+    fin = np.isfinite(z["neg2"])
+    assert rel(r["mu"][fin], z["mu"][fin]) < 1e-6
+    ev.close()

@@ -145,3 +145,11 @@ def test_mse_restatement_properties(orc):
         r = orc.corr_vector(Xt[j], X, th, 1.95)
         want = sigma2 * (1 - r @ Ri @ r + (1 - one @ Ri @ r) ** 2 / (one @ Ri @ one))
         assert abs(m[j] - max(want, 0.0)) < 1e-6 * sigma2
+
+
+@pytest.mark.parametrize("name", ["x_d20_nugget", "x_p1", "x_d1"])
+def test_oracle_bitwise_on_extra_goldens(orc, name):
+    z = np.load(os.path.join(GOLD, f"{name}.npz"))
+    r = orc.eval_batch(z["X"], z["y"], z["thetas"], float(z["p"]), float(z["nugget"]))
+    for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+        assert np.array_equal(r[k], z[k]), k

@@ -39,7 +39,7 @@ def self_disc(fast, X, y, th, p):
         return np.where(np.isfinite(a["neg2"]), np.abs(a["neg2"] - b["neg2"]) / np.abs(a["neg2"]), 0.0)
 
 
-def main():
+def main(only_extra=False):
     build()
     ref, fast = RefLib(), RefLib(fast=True)
     orc = Oracle()
@@ -106,6 +106,25 @@ def main():
              sigma2=ev["sigma2"], jitter=ev["jitter"], log_det=ev["log_det"], self_disc=disc,
              truth=truth, sens=sens)
     print("c2 done")
+
+    # ---- extra shapes: d=20 + nugget (C4-like), exponential kernel p=1, d=1 ------------
+    for name, n, d, p, nugget, B in (("x_d20_nugget", 600, 20, 1.9, 1e-8, 16),
+                                      ("x_p1", 500, 3, 1.0, 0.0, 16),
+                                      ("x_d1", 300, 1, 1.5, 0.01, 16)):
+        rng = np.random.default_rng(n * 31 + d)
+        X = ref.maximin_lhd(n, d, 17, 2000)
+        y = np.sin(3.0 * X + 0.37 * np.arange(d)).sum(1) + 0.5 * (X * X).sum(1)
+        th = ga_thetas(ref, d, 64, seed=n)[:B]
+        ev = ref.eval_batch(X, y, th, p, nugget)
+        a = fast.eval_batch(X, y, th, p, nugget, backend="reference")
+        b = fast.eval_batch(X, y, th, p, nugget, backend="parallel")
+        with np.errstate(invalid="ignore", divide="ignore"):
+            disc = np.where(np.isfinite(a["neg2"]), np.abs(a["neg2"] - b["neg2"]) / np.abs(a["neg2"]), 0.0)
+        truth, sens = orc.eval_sensitivity(X, y, th, p, ev["jitter"], nugget=nugget, reps=2)
+        np.savez(os.path.join(OUT, f"{name}.npz"), X=X, y=y, p=p, nugget=nugget, thetas=th,
+                 neg2=ev["neg2"], mu=ev["mu"], sigma2=ev["sigma2"], jitter=ev["jitter"],
+                 log_det=ev["log_det"], self_disc=disc, truth=truth, sens=sens)
+        print(name, "done", flush=True)
 
 
 if __name__ == "__main__":
