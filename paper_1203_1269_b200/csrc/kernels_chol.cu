@@ -159,8 +159,9 @@ __device__ __forceinline__ void publish_flag(int* flag, int epoch) {
 enum {
   PR_TICKET = 0, PR_GEMM, PR_ACC_STORE, PR_POTRF, PR_DIAG_STORE, PR_BORDER, PR_OFF_WAIT, PR_TRSM,
   PR_OFF_STORE, PR_TASK_END, PR_PROD_FLAGS, PR_PROD_EMPTY, PR_N_DIAG, PR_N_OFF, PR_SLABS, PR_TOTAL,
-  PR_COUNT
+  PR_FULL_WAIT, PR_COUNT_USED
 };
+constexpr int PR_COUNT = 24;
 struct Prof {
   unsigned long long* p;
   long long last;
@@ -418,7 +419,13 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
         const int stage = it % kStages;
         const uint32_t round = it / kStages;
-        mbar_wait(&full[stage], round & 1);
+        if (tid == 0 && pr.p) {
+          const long long tw = clock64();
+          mbar_wait(&full[stage], round & 1);
+          pr.p[PR_FULL_WAIT] += (unsigned long long)(clock64() - tw);
+        } else {
+          mbar_wait(&full[stage], round & 1);
+        }
         const double* As = reinterpret_cast<const double*>(smem + kOffStages + stage * kStageBytes);
         const double* Bs = diag ? As : As + SLAB_ELEMS;
         const double* Aw = As + (16 * warp + lr) * 32 + lc;
@@ -671,11 +678,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
 size_t chol_dag_smem_bytes() { return kSmemBytes; }
 
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s) {
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
-    configured = true;
-  }
+  // per-device attribute: set on every launch (cheap) so multi-device processes are correct
+  cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   const int ntasks = a.ext ? a.ext_rt * a.NT : a.nslots * a.NT * (a.NT + 1) / 2;
   const int grid = ntasks < num_sms ? ntasks : num_sms;
   cudaMemsetAsync(a.counter, 0, sizeof(int), s);

@@ -176,12 +176,8 @@ __global__ void __launch_bounds__(1024) tri_solve_kernel(const double* __restric
 void launch_tri_solve(const double* tiles, int n, int NT, const double* b, double* x, int upper,
                       cudaStream_t s) {
   const size_t smem = (size_t)n * sizeof(double);
-  static int configured_for = 0;
-  if ((int)smem > 48 * 1024 && configured_for < (int)smem) {
-    cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(smem < 227 * 1024 ? 227 * 1024 : smem));
-    configured_for = (int)smem;
-  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   tri_solve_kernel<<<1, 1024, smem, s>>>(tiles, n, b, x, upper);
 }
 

@@ -170,12 +170,8 @@ void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
   (void)work;
   if (N <= 0) return;
   const size_t smem = (size_t)n * sizeof(double);
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(mse_point_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    configured = smem;
-  }
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(mse_point_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   mse_point_kernel<<<N, 512, smem, s>>>(Xt, X, n, d, theta, p, sigma2, tiles, v, vtv, mse, bad);
 }
 

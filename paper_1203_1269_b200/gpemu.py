@@ -515,16 +515,16 @@ class ProfileEvaluator:
 
     DAG_PHASES = ("ticket", "gemm", "acc_store", "potrf", "diag_store", "border", "off_wait",
                   "trsm", "off_store", "task_end", "prod_flags", "prod_empty", "n_diag", "n_off",
-                  "slabs", "total")
+                  "slabs", "total", "full_wait")
 
     def dag_profile(self, enable: bool = True, read: bool = False):
         """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""
-        out = np.zeros(148 * 16, dtype=np.uint64) if read else None
+        out = np.zeros(148 * 24, dtype=np.uint64) if read else None
         _check(lib().gpemu_plan_dag_profile(self.handle, int(enable),
                                             None if out is None else out.ctypes.data, 0 if out is None else out.size))
         if out is None:
             return None
-        m = out.reshape(-1, 16)
+        m = out.reshape(-1, 24)
         return {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
 
     def eval_batch_device(self, theta_ptr: int, B: int, out_ptr: int):
