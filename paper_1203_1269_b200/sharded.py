@@ -100,3 +100,38 @@ def sharded_predict(model: g.GpModel, Xtest: np.ndarray, device="cpu",
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf)
     return torch.cat(parts, 0)[:N].cpu().numpy()
+
+
+def sharded_argmin(values_local: np.ndarray, slot_offset: int, device="cpu"):
+    """The final min-reduce of a sharded multistart: global (min value, lowest global slot)
+    with the reference's tie rule (strict <, earliest slot wins; likelihood.hpp:267,
+    optimizer.hpp:125-131). Two scalar all-reduces: MIN over values, then MIN over the
+    slots that attain it (NCCL's MIN cannot carry the slot alongside the value)."""
+    import torch
+    import torch.distributed as dist
+    vals = np.asarray(values_local, dtype=np.float64)
+    local_min = vals.min() if vals.size else math.inf
+    t = torch.tensor([local_min], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    gmin = float(t.item())
+    big = np.iinfo(np.int64).max
+    hits = np.nonzero(vals == gmin)[0] if vals.size else np.empty(0, dtype=np.int64)
+    s = torch.tensor([slot_offset + int(hits[0]) if hits.size else big], dtype=torch.int64,
+                     device=device)
+    dist.all_reduce(s, op=dist.ReduceOp.MIN)
+    return gmin, int(s.item())
+
+
+def sharded_multistart(thetas: np.ndarray,
+                       evaluate: Callable[[np.ndarray], Dict[str, np.ndarray]],
+                       device="cpu") -> dict:
+    """Evaluate a fixed set of candidates (a multistart) split across ranks and return the
+    global argmin, identical on every rank; no data-path collective besides the final
+    min-reduce."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(), dist.get_rank()
+    P = thetas.shape[0]
+    lo, hi = shard_range(P, world, rank)
+    rec = evaluate(thetas[lo:hi]) if hi > lo else {"neg2": np.empty(0)}
+    vmin, slot = sharded_argmin(np.asarray(rec["neg2"]), lo, device)
+    return dict(neg2=vmin, slot=slot, theta=thetas[slot].copy())

@@ -112,3 +112,39 @@ def test_sharded_fit_gloo(orc, tmp_path, world):
     L, ld, jt = orc.factorize(orc.build_corr(X, ref["theta"], 1.95))
     alpha = orc.solve_upper(L, orc.solve_lower(L, y - ref["mu"]))
     assert np.array_equal(outs[0]["yhat"], orc.predict(X, ref["theta"], 1.95, ref["mu"], alpha, Xt))
+
+
+def _ms_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    from oracle.oracle import Oracle
+    from paper_1203_1269_b200.sharded import sharded_argmin, sharded_multistart
+    orc = Oracle()
+    X, y = small_problem(orc, 50)
+    th = 10.0 ** orc.lhs_population(np.full(2, -6.0), np.full(2, np.log10(12.0)), 37, 9)
+    th[30] = th[4]  # a duplicate: the earliest slot must win
+    res = sharded_multistart(th, lambda t: orc.eval_batch(X, y, t, 1.95))
+    # ties across ranks: every rank holds the same minimum at different slots
+    v, s = sharded_argmin(np.array([3.0, 1.0, 1.0]), 100 * (rank + 1))
+    np.savez(os.path.join(out_dir, f"ms{rank}.npz"), neg2=res["neg2"], slot=res["slot"],
+             theta=res["theta"], tie=np.array([v, s]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_multistart_min_reduce(orc, tmp_path, world):
+    import torch.multiprocessing as mp
+    mp.spawn(_ms_worker, args=(world, free_port(), str(tmp_path)), nprocs=world, join=True)
+    X, y = small_problem(orc, 50)
+    th = 10.0 ** orc.lhs_population(np.full(2, -6.0), np.full(2, np.log10(12.0)), 37, 9)
+    th[30] = th[4]
+    neg2 = orc.eval_batch(X, y, th, 1.95)["neg2"]
+    want = int(np.argmin(neg2))  # numpy argmin = first occurrence, the reference's tie rule
+    for r in range(world):
+        o = np.load(tmp_path / f"ms{r}.npz")
+        assert int(o["slot"]) == want and o["neg2"] == neg2[want]
+        assert np.array_equal(o["theta"], th[want])
+        assert o["tie"][0] == 1.0 and int(o["tie"][1]) == 101  # lowest rank's lowest slot
