@@ -279,8 +279,8 @@ __device__ __forceinline__ void warp_update16(double* C, int warp, int lane, int
 __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* empty = full + kStages;
-  uint64_t* ljj_bar = empty + kStages;  // L(j,j) bulk load for the OFF-task TRSM
+  uint64_t* ljj_bar = full + kStages;  // L(j,j) bulk load for the OFF-task TRSM
+  int* stage_cnt = reinterpret_cast<int*>(ljj_bar + 1);  // warps done with each stage
   double* C = reinterpret_cast<double*>(smem + kOffC);
   double* W = reinterpret_cast<double*>(smem + kOffW);
   Misc* misc = reinterpret_cast<Misc*>(smem + kOffMisc);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+      stage_cnt[s] = 0;
     }
     mbar_init(ljj_bar, 1);
     fence_mbar_init();
@@ -395,10 +395,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           pr.lap(PR_PROD_FLAGS);
         }
         const int stage = itp % kStages;
-        const uint32_t round = itp / kStages;
-        pr.start();
-        if (round > 0) mbar_wait(&empty[stage], (round - 1) & 1);
-        pr.lap(PR_PROD_EMPTY);
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
         mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
         bulk_g2s(dst, a_tile(K) + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
@@ -406,17 +402,14 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
                    kSlabBytes, &full[stage]);
       };
+      // Prologue: the first kStages slabs. Afterwards the LAST warp to finish with a
+      // stage refills it (slab q + kStages): no warp ever blocks waiting for the others.
       if (tid == 0) {
         const long long tsave = pr.last;
-        for (int p = 0; p < kStages - 1 && p < nslab; ++p) issue(p, it + p);
+        for (int p = 0; p < kStages && p < nslab; ++p) issue(p, it + p);
         pr.last = tsave;
       }
       for (int q = 0; q < nslab; ++q, ++it) {
-        if (tid == 0 && q + kStages - 1 < nslab) {
-          const long long tsave = pr.last;
-          issue(q + kStages - 1, it + kStages - 1);
-          pr.last = tsave;
-        }
         const int stage = it % kStages;
         const uint32_t round = it / kStages;
         if (tid == 0 && pr.p) {
@@ -449,7 +442,18 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           for (int kk = 0; kk < SLAB; ++kk) wacc -= __ldcg(ub + kk) * Bs[slab_off(bc, kk)];
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (lane == 0) {
+          __threadfence_block();
+          if (atomicAdd(&stage_cnt[stage], 1) == kConsumerWarps - 1) {
+            stage_cnt[stage] = 0;
+            if (q + kStages < nslab) {
+              fence_proxy_async_shared();  // generic-proxy reads of the stage before the TMA write
+              const long long tsave = pr.last;
+              issue(q + kStages, it + kStages);
+              pr.last = tsave;
+            }
+          }
+        }
       }
       consumer_sync();  // every consumer is done reading the stage ring
       if (tid == 0) {
