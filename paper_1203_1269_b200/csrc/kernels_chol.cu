@@ -122,7 +122,8 @@ constexpr int kOffStages = 0;                           // [0, 192K)
 constexpr int kOffC = 0;                                // epilogue tile [0, 128K)
 constexpr int kOffBar = kStages * kStageBytes;          // 192K: mbarriers
 constexpr int kOffW = kOffBar + 256;                    // border w: 2 x 128 doubles
-constexpr int kOffMisc = kOffW + 2 * TILE * 8;          // task scalars
+constexpr int kOffRinvD = kOffW + 2 * TILE * 8;        // 1 / L_cc of the DIAG tile
+constexpr int kOffMisc = kOffRinvD + TILE * 8;          // task scalars
 constexpr int kSmemBytes = kOffMisc + 64;
 constexpr long long kSpinLimitCycles = 20000000000LL;  // ~10 s: declare deadlock
 constexpr int kStageLd = 18;  // row stride (doubles) of the per-warp TRSM staging block
@@ -222,9 +223,19 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 
 // Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16).
 // Returns false (uniform across the warp) on a failed pivot.
-__device__ bool potrf16(double* C, int o, int lane) {
+// a / d given r = 1/d: the rounding of a true division (a*r + one FMA residual
+// correction) without the DDIV call sequence.
+__device__ __forceinline__ double div_by(double a, double d, double r) {
+  const double x0 = a * r;
+  return fma(fma(-x0, d, a), r, x0);
+}
+
+// Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16); the
+// reciprocals of the new pivots go to rinv[o .. o+15]. Returns false (uniform across the
+// warp) on a failed pivot.
+__device__ bool potrf16(double* C, int o, int lane, double* rinv) {
   for (int c = 0; c < 16; ++c) {
-    double dval = 0.0;
+    double dval = 0.0, rval = 0.0;
     int ok = 1;
     if (lane == c) {
       double s = Cs(C, o + c, o + c);
@@ -234,15 +245,20 @@ __device__ bool potrf16(double* C, int o, int lane) {
       }
       ok = s > 0.0;  // backend.hpp:238 pivot test, NaN-safe
       dval = ok ? sqrt(s) : 0.0;
-      if (ok) Cs(C, o + c, o + c) = dval;
+      rval = ok ? 1.0 / dval : 0.0;
+      if (ok) {
+        Cs(C, o + c, o + c) = dval;
+        rinv[o + c] = rval;
+      }
     }
     dval = __shfl_sync(0xffffffffu, dval, c);
+    rval = __shfl_sync(0xffffffffu, rval, c);
     ok = __shfl_sync(0xffffffffu, ok, c);
     if (!ok) return false;
     if (lane > c && lane < 16) {
       double x = Cs(C, o + lane, o + c);
       for (int t = 0; t < c; ++t) x -= Cs(C, o + lane, o + t) * Cs(C, o + c, o + t);
-      Cs(C, o + lane, o + c) = x / dval;
+      Cs(C, o + lane, o + c) = div_by(x, dval, rval);
     }
     __syncwarp();
   }
@@ -283,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   int* stage_cnt = reinterpret_cast<int*>(ljj_bar + 1);  // warps done with each stage
   double* C = reinterpret_cast<double*>(smem + kOffC);
   double* W = reinterpret_cast<double*>(smem + kOffW);
+  double* rinvD = reinterpret_cast<double*>(smem + kOffRinvD);
   Misc* misc = reinterpret_cast<Misc*>(smem + kOffMisc);
 
   const int tid = threadIdx.x;
@@ -479,7 +496,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           for (int kb = 0; kb < 8 && ok; ++kb) {
             const int o = 16 * kb;
             if (warp == 0) {
-              if (!potrf16(C, o, lane) && lane == 0) misc->fail = 1;
+              if (!potrf16(C, o, lane, rinvD) && lane == 0) misc->fail = 1;
             }
             consumer_sync();
             if (misc->fail) {
@@ -496,7 +513,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               for (int c = 0; c < 16; ++c) {
 #pragma unroll
                 for (int tt = 0; tt < c; ++tt) x[c] -= x[tt] * Cs(C, o + c, o + tt);
-                x[c] = x[c] / Cs(C, o + c, o + c);
+                x[c] = div_by(x[c], Cs(C, o + c, o + c), rinvD[o + c]);
               }
 #pragma unroll
               for (int c = 0; c < 16; ++c) Cs(C, r, o + c) = x[c];
@@ -526,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (ok && warp < 2) {
           double* w = W + warp * TILE;
           for (int c = 0; c < TILE; ++c) {
-            const double x = w[c] / Cs(C, c, c);
+            const double x = div_by(w[c], Cs(C, c, c), rinvD[c]);
             __syncwarp();
             for (int l = c + 1 + lane; l < TILE; l += 32) w[l] -= x * Cs(C, l, c);
             if (lane == 0) w[c] = x;
