@@ -218,11 +218,7 @@ __device__ __forceinline__ int acc_off(int r, int ni, int lc) {
   return ((ni >> 2) << 12) + r * 32 + (((2 * (ni & 3) + (lc >> 1)) ^ (r & 7)) << 2) + 2 * (lc & 1);
 }
 
-// C tile accessors in shared memory (tile layout).
-__device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_off(r, c)]; }
 
-// Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16).
-// Returns false (uniform across the warp) on a failed pivot.
 // a / d given r = 1/d: the rounding of a true division (a*r + one FMA residual
 // correction) without the DDIV call sequence.
 __device__ __forceinline__ double div_by(double a, double d, double r) {
@@ -230,66 +226,211 @@ __device__ __forceinline__ double div_by(double a, double d, double r) {
   return fma(fma(-x0, d, a), r, x0);
 }
 
-// Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16); the
-// reciprocals of the new pivots go to rinv[o .. o+15]. Returns false (uniform across the
-// warp) on a failed pivot.
-__device__ bool potrf16(double* C, int o, int lane, double* rinv) {
+// ---- register-layout helpers: warp w owns rows [16w, 16w+16) as acc[2][16][2] ----------
+// (acc[mi][ni] = rows 8mi + lr, cols 8ni + 2lc + {0,1}; the "window" block is ni = 0..1)
+
+// window block (16 x 16) <-> per-warp staging St[16][kStageLd] (row r at St + r*kStageLd)
+__device__ __forceinline__ void stage_out(const double (&acc)[2][16][2], double* St, int lr, int lc) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nsub = 0; nsub < 2; ++nsub)
+      *reinterpret_cast<double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc) =
+          make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+}
+__device__ __forceinline__ void stage_in(double (&acc)[2][16][2], const double* St, int lr, int lc) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nsub = 0; nsub < 2; ++nsub) {
+      const double2 v = *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc);
+      acc[mi][nsub][0] = v.x;
+      acc[mi][nsub][1] = v.y;
+    }
+}
+
+// One lane owns one row (16 values) of a block: X = B D^-T with D dense lower [16][16]
+// (warp-uniform broadcast loads) and ri[c] = 1 / D[c][c].
+__device__ __forceinline__ void solve_row16(double (&xr)[16], const double* D, const double* ri) {
+#pragma unroll
   for (int c = 0; c < 16; ++c) {
-    double dval = 0.0, rval = 0.0;
+    xr[c] = div_by(xr[c], D[c * 16 + c], ri[c]);
+#pragma unroll
+    for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] -= xr[c] * D[c2 * 16 + c];
+  }
+}
+
+__device__ __forceinline__ void load_row16(double (&xr)[16], const double* row) {
+#pragma unroll
+  for (int c = 0; c < 16; c += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(row + c);
+    xr[c] = v.x;
+    xr[c + 1] = v.y;
+  }
+}
+__device__ __forceinline__ void store_row16(const double (&xr)[16], double* row) {
+#pragma unroll
+  for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(row + c) = make_double2(xr[c], xr[c + 1]);
+}
+
+// Negated A fragments (m8n8k4, k = window columns) of the window block, from the
+// accumulator layout by quad shuffles.
+__device__ __forceinline__ void window_afrags(const double (&acc)[2][16][2], double (&av)[2][4], int lane) {
+  const int lc = lane & 3, qbase = lane & ~3;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int src = qbase | (2 * (ks & 1) + (lc >> 1));
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const double v0 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][0], src);
+      const double v1 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][1], src);
+      av[mi][ks] = -((lc & 1) ? v1 : v0);
+    }
+  }
+}
+
+__device__ __forceinline__ void rotate_window(double (&acc)[2][16][2]) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 14; ++ni) {
+      acc[mi][ni][0] = acc[mi][ni + 2][0];
+      acc[mi][ni][1] = acc[mi][ni + 2][1];
+    }
+}
+
+// Dense panel buffer [128][16] with the 4-double chunks of row r XOR-swizzled by (r & 3).
+__device__ __forceinline__ int p_off(int r, int c) {
+  return r * 16 + ((((c >> 2) ^ (r & 3)) << 2) | (c & 3));
+}
+
+// In-register Cholesky of a 16x16 diagonal block, lane r (< 16) holding row r in xr.
+// Right-looking: column c is broadcast through colbuf. Pivot reciprocals -> rinv[0..15].
+// Returns false (uniform) on a failed pivot (backend.hpp:238).
+__device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* colbuf, double* rinv, int lane) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    double d = 0.0, r = 0.0;
     int ok = 1;
     if (lane == c) {
-      double s = Cs(C, o + c, o + c);
-      for (int t = 0; t < c; ++t) {
-        const double l = Cs(C, o + c, o + t);
-        s -= l * l;
-      }
-      ok = s > 0.0;  // backend.hpp:238 pivot test, NaN-safe
-      dval = ok ? sqrt(s) : 0.0;
-      rval = ok ? 1.0 / dval : 0.0;
-      if (ok) {
-        Cs(C, o + c, o + c) = dval;
-        rinv[o + c] = rval;
-      }
+      const double s = xr[c];
+      ok = s > 0.0;
+      d = ok ? sqrt(s) : 0.0;
+      r = ok ? 1.0 / d : 0.0;
+      xr[c] = d;
+      if (ok) rinv[c] = r;
     }
-    dval = __shfl_sync(0xffffffffu, dval, c);
-    rval = __shfl_sync(0xffffffffu, rval, c);
+    d = __shfl_sync(0xffffffffu, d, c);
+    r = __shfl_sync(0xffffffffu, r, c);
     ok = __shfl_sync(0xffffffffu, ok, c);
     if (!ok) return false;
     if (lane > c && lane < 16) {
-      double x = Cs(C, o + lane, o + c);
-      for (int t = 0; t < c; ++t) x -= Cs(C, o + lane, o + t) * Cs(C, o + c, o + t);
-      Cs(C, o + lane, o + c) = div_by(x, dval, rval);
+      xr[c] = div_by(xr[c], d, r);
+      colbuf[lane] = xr[c];
+    }
+    __syncwarp();
+    if (lane > c && lane < 16) {
+#pragma unroll
+      for (int c2 = c + 1; c2 < 16; ++c2)
+        if (c2 <= lane) xr[c2] -= xr[c] * colbuf[c2];
     }
     __syncwarp();
   }
   return true;
 }
 
-// C[rows >= r0 of warp, cols n >= n0] -= A_rows * B^T with K = 16 columns at
-// offset ko; B rows read through bfetch(row, k). Warp w owns rows [16w, 16w+16).
-template <typename BFetch>
-__device__ __forceinline__ void warp_update16(double* C, int warp, int lane, int ko, int nb_lo,
-                                              int nb_hi, BFetch bfetch) {
+// C tile accessors in shared memory (tile layout).
+__device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_off(r, c)]; }
+
+// Unblocked 16x16 Cholesky of the diagonal block at offset o (warp 0, lanes < 16).
+// Returns false (uniform across the warp) on a failed pivot.
+
+
+// DIAG-task POTRF of the 128x128 tile C (tile layout in shared memory, = R - sum L L^T):
+// blocked right-looking in the register layout. Step kb: warp kb factors its 16x16
+// diagonal block in registers (one lane per row); warps below solve their panel block
+// against it (one lane per row) and publish it to a dense panel buffer; then each updates
+// its own trailing columns with DMMA. Finished blocks are written back into C. Returns
+// false on a failed pivot (uniform). Reciprocal pivots -> rinvD[0..127].
+__device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, Misc* misc,
+                                        int warp, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
-  double a[2][4];
+  double acc[2][16][2];
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) a[mi][ks] = -Cs(C, 16 * warp + 8 * mi + lr, ko + 4 * ks + lc);
-  for (int nb = nb_lo; nb <= nb_hi; ++nb) {
-    double b[4];
+    for (int ni = 0; ni < 16; ++ni) {
+      const double2 v = *reinterpret_cast<const double2*>(C + acc_off(16 * warp + 8 * mi + lr, ni, lc));
+      acc[mi][ni][0] = v.x;
+      acc[mi][ni][1] = v.y;
+    }
+  double* Dblk = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [16][16]
+  double* P = Dblk + 256;                                                     // [128][16]
+  double* Stw = P + TILE * 16 + warp * (16 * kStageLd);                       // per warp
+  double* colbuf = P + TILE * 16 + kConsumerWarps * 16 * kStageLd;            // [16]
+  for (int kb = 0; kb < 8; ++kb) {
+    const int o = 16 * kb;
+    if (warp == kb) {
+      stage_out(acc, Stw, lr, lc);
+      __syncwarp();
+      double xr[16];
+      if (lane < 16) load_row16(xr, Stw + lane * kStageLd);
+      const bool okw = potrf_row16(xr, colbuf, rinvD + o, lane);
+      if (!okw && lane == 0) misc->fail = 1;
+      if (lane < 16) {
+        store_row16(xr, Stw + lane * kStageLd);
+        store_row16(xr, Dblk + lane * 16);
+      }
+      __syncwarp();
+      stage_in(acc, Stw, lr, lc);
+    }
+    consumer_sync();
+    if (misc->fail) return false;
+    if (warp > kb) {
+      stage_out(acc, Stw, lr, lc);
+      __syncwarp();
+      if (lane < 16) {
+        double xr[16];
+        load_row16(xr, Stw + lane * kStageLd);
+        solve_row16(xr, Dblk, rinvD + o);
+        store_row16(xr, Stw + lane * kStageLd);
+        const int r = 16 * warp + lane;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) b[ks] = bfetch(8 * nb + lr, ko + 4 * ks + lc);
+        for (int c = 0; c < 16; c += 2)
+          *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
+      }
+      __syncwarp();
+      stage_in(acc, Stw, lr, lc);
+    }
+    if (warp >= kb) {
 #pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      const int r = 16 * warp + 8 * mi + lr;
-      double2* p = reinterpret_cast<double2*>(&Cs(C, r, 8 * nb + 2 * lc));
-      double2 acc = *p;
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) dmma884(acc.x, acc.y, a[mi][ks], b[ks]);
-      *p = acc;
+        for (int nsub = 0; nsub < 2; ++nsub)
+          *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
+              make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+    }
+    consumer_sync();  // the panel buffer is complete
+    if (warp > kb) {
+      double av[2][4];
+      window_afrags(acc, av, lane);
+      const int nlast = 2 * (warp - kb) + 1;  // the warp's own diagonal block
+#pragma unroll
+      for (int nb = 2; nb < 16; ++nb) {
+        if (nb <= nlast) {
+          const int prow = o + 8 * nb + lr;
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks) {
+            const double b = P[p_off(prow, 4 * ks + lc)];
+            dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
+            dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
+          }
+        }
+      }
+      rotate_window(acc);
     }
   }
+  return true;
 }
 
 __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
@@ -481,7 +622,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
 
       if (diag) {
         // ------------------------------ DIAG ------------------------------
-        // accumulators (= R - sum L L^T) -> C (tile layout)
+        // accumulators (= R - sum L L^T) -> C (tile layout); the POTRF runs in its own
+        // (non-inlined) function so its register pressure stays out of the mainloop
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -493,40 +635,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         bool ok = !skip;
         if (!skip) {
           W[brow * TILE + bc] = wacc;
-          for (int kb = 0; kb < 8 && ok; ++kb) {
-            const int o = 16 * kb;
-            if (warp == 0) {
-              if (!potrf16(C, o, lane, rinvD) && lane == 0) misc->fail = 1;
-            }
-            consumer_sync();
-            if (misc->fail) {
-              ok = false;
-              break;
-            }
-            // panel rows below the 16x16 block
-            const int r = o + 16 + tid;
-            if (r < TILE) {
-              double x[16];
-#pragma unroll
-              for (int c = 0; c < 16; ++c) x[c] = Cs(C, r, o + c);
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-#pragma unroll
-                for (int tt = 0; tt < c; ++tt) x[c] -= x[tt] * Cs(C, o + c, o + tt);
-                x[c] = div_by(x[c], Cs(C, o + c, o + c), rinvD[o + c]);
-              }
-#pragma unroll
-              for (int c = 0; c < 16; ++c) Cs(C, r, o + c) = x[c];
-            }
-            consumer_sync();
-            // trailing lower update with the 16-wide panel (DMMA)
-            if (16 * warp >= o + 16) {
-              warp_update16(C, warp, lane, o, (o + 16) >> 3, 2 * warp + 1,
-                            [&](int row, int k) { return Cs(C, row, k); });
-            }
-            consumer_sync();
-          }
+          ok = diag_potrf(smem, C, rinvD, misc, warp, lane);
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
+          consumer_sync();
         }
         if (tid == 0) pr.lap(PR_POTRF);
         // L(j,j) -> HBM, then publish
@@ -593,64 +704,24 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             Dd[q] = cc <= rr ? Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)] : 0.0;
           }
           consumer_sync();
-          const int qbase = lane & ~3;
           for (int cb = 0; cb < 8; ++cb) {
             const int o = 16 * cb;
             // (a) columns o..o+15 (acc[mi][0..1], rotated window): through the warp's
             // staging block so lane r < 16 owns row r and substitutes in registers
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-              for (int nsub = 0; nsub < 2; ++nsub)
-                *reinterpret_cast<double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc) =
-                    make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+            stage_out(acc, St, lr, lc);
             __syncwarp();
             if (lane < 16) {
               double xr[16];
-              double* row = St + lane * kStageLd;
-#pragma unroll
-              for (int c = 0; c < 16; c += 2) {
-                const double2 v = *reinterpret_cast<const double2*>(row + c);
-                xr[c] = v.x;
-                xr[c + 1] = v.y;
-              }
-              const double* D = Dd + cb * 256;
-              const double* ri = rinv + o;
-#pragma unroll
-              for (int c = 0; c < 16; ++c) {
-                const double rcc = ri[c], lcc = D[c * 16 + c];
-                const double x0 = xr[c] * rcc;
-                xr[c] = fma(fma(-x0, lcc, xr[c]), rcc, x0);
-#pragma unroll
-                for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] -= xr[c] * D[c2 * 16 + c];
-              }
-#pragma unroll
-              for (int c = 0; c < 16; c += 2)
-                *reinterpret_cast<double2*>(row + c) = make_double2(xr[c], xr[c + 1]);
+              load_row16(xr, St + lane * kStageLd);
+              solve_row16(xr, Dd + cb * 256, rinv + o);
+              store_row16(xr, St + lane * kStageLd);
             }
             __syncwarp();
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-              for (int nsub = 0; nsub < 2; ++nsub) {
-                const double2 v =
-                    *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc);
-                acc[mi][nsub][0] = v.x;
-                acc[mi][nsub][1] = v.y;
-              }
+            stage_in(acc, St, lr, lc);
             // (b) acc[:, 2..] -= X_block * L(j,j)[rows right of the block, block cols]^T
             if (cb < 7) {
               double av[2][4];
-#pragma unroll
-              for (int ks = 0; ks < 4; ++ks) {
-                const int src = qbase | (2 * (ks & 1) + (lc >> 1));
-#pragma unroll
-                for (int mi = 0; mi < 2; ++mi) {
-                  const double v0 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][0], src);
-                  const double v1 = __shfl_sync(0xffffffffu, acc[mi][ks >> 1][1], src);
-                  av[mi][ks] = -((lc & 1) ? v1 : v0);
-                }
-              }
+              window_afrags(acc, av, lane);
 #pragma unroll
               for (int nb = 2; nb < 16; ++nb) {
                 if (nb < 16 - 2 * cb) {
@@ -672,13 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
                 __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, 2 * cb + nsub, lc)),
                        make_double2(acc[mi][nsub][0], acc[mi][nsub][1]));
             // (d) rotate the window by one 16-column block
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-              for (int ni = 0; ni < 14; ++ni) {
-                acc[mi][ni][0] = acc[mi][ni + 2][0];
-                acc[mi][ni][1] = acc[mi][ni + 2][1];
-              }
+            rotate_window(acc);
           }
           if (tid == 0) pr.lap(PR_TRSM);
         }
