@@ -40,9 +40,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4096)
-    ap.add_argument("--d", type=int, default=10)
-    ap.add_argument("--p", type=float, default=1.95)
+    # (long names: torchrun would take --n / --d / --p as abbreviations of its own options)
+    ap.add_argument("--size", dest="n", type=int, default=4096)
+    ap.add_argument("--dims", dest="d", type=int, default=10)
+    ap.add_argument("--power", dest="p", type=float, default=1.95)
     ap.add_argument("--batch", type=int, default=100)
     ap.add_argument("--seed", type=int, default=20120306)
     ap.add_argument("--no-cpu-baseline", action="store_true")
