@@ -745,7 +745,7 @@ int gpemu_plan_phase_ms(gpemu_plan* pl, int phase, double* total_ms, int* launch
 int gpemu_plan_dag_profile(gpemu_plan* pl, int enable, uint64_t* out, size_t out_len) {
   GPEMU_GUARD_BEGIN
   if (!pl) return set_error(GPEMU_VALIDATION, "null plan");
-  const size_t len = (size_t)pl->ctx->num_sms * 24;
+  const size_t len = (size_t)pl->ctx->num_sms * 24 + 256;
   if (out && pl->dag_prof.p) {
     ck(cudaStreamSynchronize(pl->ctx->stream), "dag_profile");
     ck(cudaMemcpy(out, pl->dag_prof.p, std::min(out_len, len) * sizeof(uint64_t), cudaMemcpyDeviceToHost),

@@ -539,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         const int K = p >> 2, sq = p & 3;
         if (sq == 0) {
           pr.start();
+          const long long tw0 = (pr.p != nullptr || a.prof != nullptr) ? clock64() : 0;
           if (ext) {
             wait_flag(&a.ext_flags[(size_t)It * NT + K], epoch, a.error);
           } else {
@@ -550,6 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             }
           }
           fence_proxy_async_global();
+          if (a.prof) atomicAdd(a.prof + (size_t)gridDim.x * PR_COUNT + (diag ? 128 : 0) + j,
+                                (unsigned long long)(clock64() - tw0));
           pr.lap(PR_PROD_FLAGS);
         }
         const int stage = itp % kStages;
