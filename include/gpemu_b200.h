@@ -167,6 +167,17 @@ GPEMU_API int gpemu_ga_status(const gpemu_ga* ga, int* generation, int* done, do
                     double* best_theta, int* stash_generation, int* stash_slot,
                     double* trace_best /* generations */, double* trace_genes /* generations x d */);
 
+/* The bench protocol's post-GA polish (bench.hpp:302-383 detail::refine_fit): coordinate-
+ * wise golden-section search in log10(theta), +-0.25 around the incumbent, exactly `budget`
+ * sequential single-candidate evaluations. theta_out / neg2_out: the polished incumbent;
+ * model_out (nullable) receives the model rebuilt at it when it improved on neg2_fit,
+ * else NULL; scalars[4] = {neg2, mu, sigma2, jitter} and alpha[n] (both nullable) are
+ * filled for the rebuilt model only. */
+GPEMU_API int gpemu_refine_fit(gpemu_plan* plan, const double* lo, const double* hi,
+                               const double* theta_fit, double neg2_fit, int budget,
+                               double* theta_out, double* neg2_out, int* evals_out,
+                               gpemu_model** model_out, double* scalars, double* alpha);
+
 /* model_at_theta (likelihood.hpp:216-237). scalars: neg2, mu, sigma2, jitter. */
 GPEMU_API int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,
                          double* scalars, double* alpha);

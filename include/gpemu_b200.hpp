@@ -191,6 +191,27 @@ inline FitResult fit_gp_detailed(BatchEvaluator& ev, std::span<const double> lo,
   return out;
 }
 
+// The bench protocol's post-GA polish (bench.hpp:302-383 detail::refine_fit): `budget`
+// golden-section evaluations around fit.theta; fit (theta, scalars, alpha, model) is replaced
+// when -2logL improves. Returns the extra evaluations (budget, +1 for the model rebuild).
+inline std::size_t refine_fit(BatchEvaluator& ev, FitResult& fit, std::span<const double> lo,
+                              std::span<const double> hi, int budget = 20) {
+  std::vector<double> theta(ev.d()), alpha(ev.n());
+  double neg2 = 0.0, sc[4] = {};
+  int used = 0;
+  gpemu_model* m = nullptr;
+  check(gpemu_refine_fit(ev.get(), lo.data(), hi.data(), fit.theta.data(), fit.neg2_log_lik,
+                         budget, theta.data(), &neg2, &used, &m, sc, alpha.data()));
+  if (!m) return static_cast<std::size_t>(used);
+  fit.model = Model(m);
+  fit.theta = std::move(theta);
+  fit.alpha = std::move(alpha);
+  fit.neg2_log_lik = sc[0];
+  fit.mu_hat = sc[1];
+  fit.sigma2_hat = sc[2];
+  return static_cast<std::size_t>(used) + 1;
+}
+
 // predict (predictor.hpp:20-50); mse (optional) is the kriging variance.
 inline std::vector<double> predict(const Model& m, std::span<const double> Xtest, std::size_t d,
                                    std::vector<double>* mse = nullptr) {

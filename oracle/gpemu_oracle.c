@@ -931,3 +931,101 @@ int orc_profile_sensitivity(const double* X, const double* y, size_t n, size_t d
   free(v);
   return 0;
 }
+
+/* ======================================================================== */
+/* bench.hpp:302-383 detail::refine_fit (coordinate-wise golden-section polish) */
+/* ======================================================================== */
+typedef struct {
+  const double* table;
+  const double* y;
+  size_t n, d;
+  double nugget;
+  int kind;
+  double* R;
+  double* L;
+  double* theta;
+  int used;
+  double best_value;
+  double* best_genes;
+} refine_ctx;
+
+static double refine_eval(refine_ctx* c, const double* genes) {
+  for (size_t k = 0; k < c->d; ++k) c->theta[k] = pow(10.0, genes[k]);
+  ++c->used;
+  orc_profile ev;
+  orc_profile_eval_table(c->table, c->y, c->n, c->d, c->nugget, c->theta, c->kind, &ev, c->L, c->R);
+  const double v = ev.neg2_log_lik;
+  if (v < c->best_value) {
+    c->best_value = v;
+    memcpy(c->best_genes, genes, c->d * sizeof(double));
+  }
+  return v;
+}
+
+int orc_refine_fit(const double* X, const double* y, size_t n, size_t d, double p, double nugget,
+                   const double* lo, const double* hi, const double* theta_fit, double neg2_fit,
+                   int budget, int kind, double* theta_out, double* neg2_out, int* used_out) {
+  const size_t pairs = n * (n - 1) / 2;
+  refine_ctx c;
+  memset(&c, 0, sizeof(c));
+  double* table = (double*)malloc((pairs * d > 0 ? pairs * d : 1) * sizeof(double));
+  c.R = (double*)malloc(n * n * sizeof(double));
+  c.L = (double*)malloc(n * n * sizeof(double));
+  c.theta = (double*)malloc(d * sizeof(double));
+  c.best_genes = (double*)malloc(d * sizeof(double));
+  double* g = (double*)malloc(d * sizeof(double));
+  if (!table || !c.R || !c.L || !c.theta || !c.best_genes || !g) return -2;
+  orc_corr_table(X, n, d, p, table);
+  c.table = table;
+  c.y = y;
+  c.n = n;
+  c.d = d;
+  c.nugget = nugget;
+  c.kind = kind;
+  for (size_t k = 0; k < d; ++k) c.best_genes[k] = log10(theta_fit[k]);
+  c.best_value = neg2_fit;
+  const double kInvPhi = 0.6180339887498949, kHalfWidth = 0.25;
+  size_t k = 0;
+  while (c.used < budget) {
+    memcpy(g, c.best_genes, d * sizeof(double));
+    const double blo = log10(lo[k]), bhi = log10(hi[k]);
+    double a = c.best_genes[k] - kHalfWidth, b = c.best_genes[k] + kHalfWidth;
+    double lo_k = blo > a ? blo : a;
+    double hi_k = bhi < b ? bhi : b;
+    double x1 = hi_k - kInvPhi * (hi_k - lo_k);
+    double x2 = lo_k + kInvPhi * (hi_k - lo_k);
+    g[k] = x1;
+    double f1 = refine_eval(&c, g);
+    if (c.used >= budget) break;
+    g[k] = x2;
+    double f2 = refine_eval(&c, g);
+    for (int step = 0; step < 2 && c.used < budget; ++step) {
+      if (f1 <= f2) {
+        hi_k = x2;
+        x2 = x1;
+        f2 = f1;
+        x1 = hi_k - kInvPhi * (hi_k - lo_k);
+        g[k] = x1;
+        f1 = refine_eval(&c, g);
+      } else {
+        lo_k = x1;
+        x1 = x2;
+        f1 = f2;
+        x2 = lo_k + kInvPhi * (hi_k - lo_k);
+        g[k] = x2;
+        f2 = refine_eval(&c, g);
+      }
+    }
+    k = (k + 1) % d;
+  }
+  for (size_t q = 0; q < d; ++q) theta_out[q] = pow(10.0, c.best_genes[q]);
+  *neg2_out = c.best_value;
+  *used_out = c.used;
+  free(table);
+  free(c.R);
+  free(c.L);
+  free(c.theta);
+  free(c.best_genes);
+  free(g);
+  return 0;
+}

@@ -130,6 +130,13 @@ int orc_fit(const double* X, const double* y, size_t n, size_t d, double p, doub
             double* theta_hat, orc_fit_result* res, double* alpha /* n */, double* L /* n*n or NULL */,
             double* trace_best /* generations */, double* trace_genes /* generations*d */);
 
+/* bench.hpp:302-383 detail::refine_fit: coordinate-wise golden-section polish of theta
+ * around a fitted optimum with exactly `budget` extra evaluations (the model rebuild at the
+ * refined theta is left to the caller). theta_out / neg2_out = the polished incumbent. */
+int orc_refine_fit(const double* X, const double* y, size_t n, size_t d, double p, double nugget,
+                   const double* lo, const double* hi, const double* theta_fit, double neg2_fit,
+                   int budget, int kind, double* theta_out, double* neg2_out, int* used_out);
+
 /* ---- predictor.hpp ------------------------------------------------------ */
 /* predict (:20-50): yhat_j = mu + dot_accumulate(r_j, alpha). */
 int orc_predict(const double* X, size_t n, size_t d, const double* theta, double p, double mu,

@@ -93,6 +93,8 @@ class Oracle:
                                           _dp, _dp]
         L.orc_profile_sensitivity.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp,
                                               _sz, _dp, C.c_int, _u64, _dp, _dp]
+        L.orc_refine_fit.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _dp, _dp,
+                                     C.c_double, C.c_int, C.c_int, _dp, _dp, C.POINTER(C.c_int)]
         L.orc_sspe.restype = C.c_double
         L.orc_sspe.argtypes = [_dp, _dp, _sz]
 
@@ -236,6 +238,20 @@ class Oracle:
                     jitter_max=res.jitter_max, jitter_used=res.jitter_used, log_det=res.log_det,
                     alpha=alpha, L=L, trace_best=tb, trace_genes=tg)
 
+    def refine_fit(self, X, y, theta_fit, neg2_fit, p=1.95, nugget=0.0, lo=1e-6, hi=12.0,
+                   budget=20, kind=1):
+        """bench.hpp:302-383 golden-section polish -> (theta, neg2, evals used)."""
+        X, y, th = _f64(X), _f64(y), _f64(theta_fit)
+        n, d = X.shape
+        lo = _f64(np.broadcast_to(lo, (d,)))
+        hi = _f64(np.broadcast_to(hi, (d,)))
+        out, nv, used = np.empty(d), C.c_double(), C.c_int()
+        rc = self.lib.orc_refine_fit(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(lo), _ptr(hi), _ptr(th),
+                                     neg2_fit, budget, kind, _ptr(out), C.byref(nv), C.byref(used))
+        if rc != 0:
+            raise MemoryError("oracle refine_fit failed")
+        return out, nv.value, used.value
+
     # -- predictor ----------------------------------------------------------
     def predict(self, X, theta, p, mu, alpha, Xtest):
         X, theta, alpha, Xtest = _f64(X), _f64(theta), _f64(alpha), _f64(Xtest)
@@ -291,6 +307,8 @@ class RefLib:
                                            cs, C.c_uint, _dp, _dp, _dp]
         L.ref_fit.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _dp, C.c_int,
                               C.c_int, _u64, cs, C.c_uint, _dp, _dp, _dp, _dp, _dp]
+        L.ref_fit_refine.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _dp, C.c_int,
+                                     C.c_int, _u64, C.c_int, C.c_uint, _dp, _dp, _dp]
         L.ref_model_predict.argtypes = [_dp, _dp, _sz, _sz, _dp, C.c_double, C.c_double, cs,
                                         C.c_uint, _dp, _sz, _dp, _dp, _dp]
 
@@ -393,6 +411,19 @@ class RefLib:
                                      _ptr(theta), _ptr(sc), _ptr(alpha), _ptr(tb), _ptr(tg)))
         return dict(theta=theta, neg2=sc[0], mu=sc[1], sigma2=sc[2], jitter_max=sc[3], alpha=alpha,
                     trace_best=tb, trace_genes=tg)
+
+    def fit_refine(self, X, y, p=1.95, nugget=0.0, lo=1e-6, hi=12.0, population=100,
+                   generations=20, seed=0, budget=20, threads=1):
+        """fit_gp_detailed + bench.hpp refine_fit -> (theta_fit, neg2_fit, theta_ref, neg2_ref, extra)."""
+        X, y = _f64(X), _f64(y)
+        n, d = X.shape
+        lo = _f64(np.broadcast_to(lo, (d,)))
+        hi = _f64(np.broadcast_to(hi, (d,)))
+        tf, tr, sc = np.empty(d), np.empty(d), np.empty(3)
+        self._check(self.lib.ref_fit_refine(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(lo), _ptr(hi),
+                                            population, generations, seed, budget, threads, _ptr(tf),
+                                            _ptr(tr), _ptr(sc)))
+        return tf, sc[0], tr, sc[1], int(sc[2])
 
     def model_predict(self, X, y, theta, p, nugget, Xtest, backend="parallel", threads=1):
         X, y, theta = _f64(X), _f64(y), _f64(theta)

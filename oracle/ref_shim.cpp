@@ -221,6 +221,36 @@ REF_API int ref_fit(const double* X, const double* y, std::size_t n, std::size_t
   REF_CATCH
 }
 
+// fit_gp_detailed followed by the bench's golden-section polish (bench.hpp:302-383).
+REF_API int ref_fit_refine(const double* X, const double* y, std::size_t n, std::size_t d, double p,
+                           double nugget, const double* lo, const double* hi, int population,
+                           int generations, std::uint64_t seed, int budget, unsigned threads,
+                           double* theta_fit, double* theta_refined,
+                           double* scalars /*neg2 fit, neg2 refined, extra evals*/) {
+  REF_TRY
+  auto be = make_backend<double>("parallel", threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  FitConfig cfg;
+  cfg.backend = "parallel";
+  cfg.ga.population = population;
+  cfg.ga.generations = generations;
+  cfg.seed = seed;
+  cfg.p = p;
+  cfg.nugget = nugget;
+  cfg.theta_bounds.resize(d);
+  for (std::size_t k = 0; k < d; ++k) cfg.theta_bounds[k] = {lo[k], hi[k]};
+  auto fit = fit_gp_detailed(data, cfg, *be);
+  for (std::size_t k = 0; k < d; ++k) theta_fit[k] = fit.model.params.theta[k];
+  scalars[0] = fit.model.neg2_log_lik;
+  std::uint64_t extra = 0;
+  detail::refine_fit(fit, data, cfg, *be, budget, &extra);
+  for (std::size_t k = 0; k < d; ++k) theta_refined[k] = fit.model.params.theta[k];
+  scalars[1] = fit.model.neg2_log_lik;
+  scalars[2] = static_cast<double>(extra);
+  return 0;
+  REF_CATCH
+}
+
 // model_at_theta + predict (predictor.hpp:20-50).
 REF_API int ref_model_predict(const double* X, const double* y, std::size_t n, std::size_t d,
                       const double* theta, double p, double nugget, const char* backend,

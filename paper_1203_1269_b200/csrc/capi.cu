@@ -1030,6 +1030,101 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
   GPEMU_GUARD_END
 }
 
+// bench.hpp:302-383 detail::refine_fit: coordinate-wise golden-section polish, `budget`
+// sequential single-candidate device evaluations; on improvement the model is rebuilt at
+// the refined theta (one more evaluation + alpha, as bench.hpp:363-382).
+int gpemu_refine_fit(gpemu_plan* pl, const double* lo, const double* hi, const double* theta_fit,
+                     double neg2_fit, int budget, double* theta_out, double* neg2_out,
+                     int* evals_out, gpemu_model** model_out, double* scalars, double* alpha) {
+  GPEMU_GUARD_BEGIN
+  if (!pl || !lo || !hi || !theta_fit) return set_error(GPEMU_VALIDATION, "refine_fit: null argument");
+  const int d = pl->d;
+  for (int k = 0; k < d; ++k)
+    if (!(lo[k] > 0.0) || !(lo[k] < hi[k])) return set_error(GPEMU_VALIDATION, "FitConfig: theta bounds require 0 < lower < upper");
+  cudaStream_t s = pl->ctx->stream;
+  std::vector<double> best(d), g(d), theta(d);
+  for (int k = 0; k < d; ++k) best[k] = std::log10(theta_fit[k]);
+  double best_value = neg2_fit;
+  int used = 0;
+  int rc = GPEMU_OK;
+  auto eval_genes = [&](const std::vector<double>& genes) -> double {
+    for (int k = 0; k < d; ++k) theta[k] = std::pow(10.0, genes[k]);
+    ++used;
+    ck(cudaMemcpyAsync(pl->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+    rc = run_batch(pl, 1);
+    if (rc) return INFINITY;
+    download_records(pl, 1);
+    const double v = pl->h_out[REC_NEG2];
+    if (v < best_value) {
+      best_value = v;
+      best = genes;
+    }
+    return v;
+  };
+  constexpr double kInvPhi = 0.6180339887498949;
+  constexpr double kHalfWidth = 0.25;  // log10 units around the incumbent
+  int k = 0;
+  while (used < budget) {
+    g = best;
+    double a = std::max(std::log10(lo[k]), best[k] - kHalfWidth);
+    double b = std::min(std::log10(hi[k]), best[k] + kHalfWidth);
+    double x1 = b - kInvPhi * (b - a);
+    double x2 = a + kInvPhi * (b - a);
+    g[k] = x1;
+    double f1 = eval_genes(g);
+    if (rc) return rc;
+    if (used >= budget) break;
+    g[k] = x2;
+    double f2 = eval_genes(g);
+    if (rc) return rc;
+    for (int step = 0; step < 2 && used < budget; ++step) {
+      if (f1 <= f2) {
+        b = x2;
+        x2 = x1;
+        f2 = f1;
+        x1 = b - kInvPhi * (b - a);
+        g[k] = x1;
+        f1 = eval_genes(g);
+      } else {
+        a = x1;
+        x1 = x2;
+        f1 = f2;
+        x2 = a + kInvPhi * (b - a);
+        g[k] = x2;
+        f2 = eval_genes(g);
+      }
+      if (rc) return rc;
+    }
+    k = (k + 1) % d;
+  }
+  for (int q = 0; q < d; ++q) theta[q] = std::pow(10.0, best[q]);
+  if (theta_out) std::copy(theta.begin(), theta.end(), theta_out);
+  if (neg2_out) *neg2_out = best_value;
+  if (evals_out) *evals_out = used;
+  if (model_out) {
+    *model_out = nullptr;
+    if (best_value < neg2_fit) {
+      ck(cudaMemcpyAsync(pl->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+      rc = run_batch(pl, 1);
+      if (rc) return rc;
+      download_records(pl, 1);
+      if (std::isfinite(pl->h_out[REC_NEG2]) && pl->h_out[REC_NEG2] < neg2_fit) {
+        gpemu_model* m = make_model(pl, 0, theta.data(), pl->h_out.data());
+        if (scalars) {
+          scalars[0] = m->neg2;
+          scalars[1] = m->mu;
+          scalars[2] = m->sigma2;
+          scalars[3] = m->jitter;
+        }
+        if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+        *model_out = m;
+      }
+    }
+  }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
 int gpemu_model_at_theta(gpemu_plan* pl, const double* theta, gpemu_model** model_out,
                          double* scalars, double* alpha) {
   GPEMU_GUARD_BEGIN

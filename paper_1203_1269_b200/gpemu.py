@@ -74,7 +74,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_eval_batch_device", "gpemu_plan_last_factor", "gpemu_fit", "gpemu_model_at_theta",
     "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
-    "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status",
+    "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
 )
 
 
@@ -135,6 +135,8 @@ def lib():
     L.gpemu_fit.argtypes = [_vp, _dp, _dp, C.POINTER(_GaConfigC), C.c_uint64,
                             C.POINTER(_FitResultC), _dp, _dp, _dp, _dp, C.POINTER(_vp)]
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]
+    L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
+                                   C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_destroy.argtypes = [_vp]
     L.gpemu_predict.argtypes = [_vp, _dp, _sz, _dp, _dp]
     _LIB = L
@@ -713,6 +715,40 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
     finally:
         if own:
             ev.close()
+
+
+def refine_fit(fit: FitResult, data: Dataset, cfg: FitConfig, backend: Backend,
+               budget: int = 20) -> int:
+    """bench.hpp:302-383 detail::refine_fit on the device: golden-section polish of the
+    fitted theta with exactly `budget` extra evaluations; the model in `fit` is replaced when
+    the polish improves -2logL. Returns the number of extra evaluations (budget, +1 when the
+    model was rebuilt), as the reference's extra_evals."""
+    d = data.d()
+    bounds = cfg.bounds_for(d)
+    lo = _f64([b[0] for b in bounds])
+    hi = _f64([b[1] for b in bounds])
+    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=1)
+    try:
+        th = np.empty(d)
+        sc = np.empty(4)
+        alpha = np.empty(data.n())
+        nv, used, mh = C.c_double(), C.c_int(), _vp()
+        _check(lib().gpemu_refine_fit(ev.handle, _p(lo), _p(hi), _p(_f64(fit.model.params.theta)),
+                                      float(fit.model.neg2_log_lik), int(budget), _p(th),
+                                      C.byref(nv), C.byref(used), C.byref(mh), _p(sc), _p(alpha)))
+        extra = used.value
+        if mh.value:
+            extra += 1
+            fit.model.close()
+            fit.model = GpModel(mh, data, Hyperparameters(list(th), cfg.p, cfg.nugget),
+                                float(sc[1]), float(sc[2]), float(sc[0]), alpha, backend.ctx)
+        led = backend.ledger()
+        led.add_r_build(extra)
+        led.add_factorization(extra)
+        led.add_triangular_solves(2 * extra + (2 if mh.value else 0))
+        return extra
+    finally:
+        ev.close()
 
 
 def fit_gp(data: Dataset, cfg: FitConfig, backend: Backend) -> GpModel:

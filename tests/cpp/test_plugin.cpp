@@ -147,6 +147,27 @@ int main() {
   for (std::size_t j = 0; j < ph.size(); ++j) worst = std::max(worst, std::abs(pp[j] - ph[j]));
   CHECK(worst < 1e-6);
 
+  // bench.hpp:302-383 refine_fit: the reference's own polish through the plugin
+  // (cfg.backend = "accelerated") and gpemu_b200::refine_fit both reach the reference's
+  // polished theta bitwise.
+  {
+    auto fr_ref = fit_gp_detailed(data, cfg, *par);
+    std::uint64_t extra_ref = 0;
+    detail::refine_fit(fr_ref, data, cfg, *par, 20, &extra_ref);
+    FitConfig cfg_acc = cfg;
+    cfg_acc.backend = "accelerated";
+    auto fr_acc = fit_gp_detailed(data, cfg_acc, *acc);
+    std::uint64_t extra_acc = 0;
+    detail::refine_fit(fr_acc, data, cfg_acc, *acc, 20, &extra_acc);
+    CHECK(fr_acc.model.params.theta == fr_ref.model.params.theta);
+    CHECK(extra_acc == extra_ref);
+    auto bf2 = gpemu_b200::fit_gp_detailed(bev, lo, hi, ga, 4);
+    const std::size_t extra_dev = gpemu_b200::refine_fit(bev, bf2, lo, hi, 20);
+    CHECK(bf2.theta == fr_ref.model.params.theta);
+    CHECK(extra_dev == extra_ref);
+    CHECK(rel_diff(bf2.neg2_log_lik, fr_ref.model.neg2_log_lik) < 1e-8);
+  }
+
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
 }

@@ -251,6 +251,44 @@ def test_fit_c1_argmin_bitwise(g, ctx, orc):
     assert np.all(mse >= 0.0)
 
 
+def test_refine_fit_bitwise(g, ctx):
+    """bench.hpp:302-383: device GA fit + golden-section polish reproduce the reference's
+    fitted and polished theta bitwise (tests/golden/refine.npz); -2logL within 1e-9."""
+    z = np.load(os.path.join(GOLD, "refine.npz"))
+    be = g.Backend(ctx)
+    for k in range(int(z["ncases"])):
+        X, y, p = z[f"X_{k}"], z[f"y_{k}"], float(z[f"p_{k}"])
+        P, G, seed = (int(v) for v in z[f"ga_{k}"])
+        data = g.new_dataset(X, y)
+        cfg = g.FitConfig(ga=g.GaConfig(population=P, generations=G), seed=seed, p=p)
+        fr = g.fit_gp_detailed(data, cfg, be)
+        assert np.array_equal(np.array(fr.model.params.theta), z[f"theta_fit_{k}"]), k
+        extra = g.refine_fit(fr, data, cfg, be)
+        assert extra == int(z[f"extra_{k}"])
+        assert np.array_equal(np.array(fr.model.params.theta), z[f"theta_ref_{k}"]), k
+        assert rel(fr.model.neg2_log_lik, z[f"neg2_ref_{k}"]) <= 1e-9
+        yhat = g.predict(fr.model, X[:10])  # the rebuilt model interpolates
+        assert np.max(np.abs(yhat - y[:10])) <= 1e-6 * np.abs(y).max()
+
+
+@pytest.mark.parametrize("name", ["c2fit", "c3fit"])
+def test_fit_large_argmin_bitwise(g, ctx, name):
+    """Full GA (100x20) at C2 / C3 sizes: theta-hat and the per-generation best genes are
+    bitwise the reference's (tests/golden/<name>.npz, tools/make_golden_fit.py)."""
+    path = os.path.join(GOLD, name + ".npz")
+    if not os.path.exists(path):
+        pytest.skip(name + " golden not generated")
+    z = np.load(path)
+    data = g.new_dataset(z["X"], z["y"])
+    cfg = g.FitConfig(ga=g.GaConfig(population=100, generations=20), seed=0, p=float(z["p"]))
+    fr = g.fit_gp_detailed(data, cfg, g.Backend(ctx))
+    assert np.array_equal(np.array(fr.model.params.theta), z["theta"])
+    assert np.array_equal(np.array([r.best_point for r in fr.trace.generations]), z["trace_genes"])
+    assert rel(np.array([r.best_value for r in fr.trace.generations]), z["trace_best"]) <= 1e-9
+    assert rel(fr.model.neg2_log_lik, z["neg2"]) <= 1e-9
+    assert fr.jitter_max == z["jitter_max"]
+
+
 def test_predict_and_mse_vs_oracle(g, ctx, orc):
     z = np.load(os.path.join(GOLD, "c1p195.npz"))
     X, y = z["X"], z["y"]

@@ -153,3 +153,18 @@ def test_oracle_bitwise_on_extra_goldens(orc, name):
     r = orc.eval_batch(z["X"], z["y"], z["thetas"], float(z["p"]), float(z["nugget"]))
     for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
         assert np.array_equal(r[k], z[k]), k
+
+
+def test_oracle_refine_fit_golden(orc):
+    """bench.hpp:302-383 refine_fit: the oracle's GA fit and golden-section polish reproduce the
+    reference's theta / -2logL bitwise (tests/golden/refine.npz, tools/make_golden_refine.py)."""
+    z = np.load(os.path.join(GOLD, "refine.npz"))
+    for k in range(int(z["ncases"])):
+        X, y, p = z[f"X_{k}"], z[f"y_{k}"], float(z[f"p_{k}"])
+        P, G, seed = (int(v) for v in z[f"ga_{k}"])
+        f = orc.fit(X, y, p=p, population=P, generations=G, seed=seed)
+        assert np.array_equal(f["theta"], z[f"theta_fit_{k}"]) and f["neg2"] == z[f"neg2_fit_{k}"]
+        th, nv, used = orc.refine_fit(X, y, f["theta"], f["neg2"], p=p)
+        assert used == 20 and int(z[f"extra_{k}"]) == 21
+        assert np.array_equal(th, z[f"theta_ref_{k}"]), k
+        assert nv == z[f"neg2_ref_{k}"], k
