@@ -20,3 +20,18 @@ def test_reference_plugin_on_b200():
     r = subprocess.run([BIN], capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-2000:])
     assert r.returncode == 0 and "ALL PASSED" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_bench_sweep_on_b200(tmp_path):
+    """bench.hpp:436-519 sweep with "accelerated" cells on the batched device path
+    (include/gpemu_b200_bench.hpp) vs the reference's own cells: same rows, CSV contract."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    exe = os.path.join(HERE, "cpp", "test_bench")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/test_bench not built (needs /root/reference at build time)")
+    r = subprocess.run([exe, str(tmp_path / "sweep.csv")], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-6000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout
