@@ -13,6 +13,7 @@
 // exp/log are CUDA libdevice (<= 1 ulp from glibc): R matches to ~1e-16, not bitwise.
 #include <cuda_runtime.h>
 
+#include "fastmath.cuh"
 #include "kernels.h"
 #include "layout.cuh"
 
@@ -72,9 +73,9 @@ constexpr int kAsmSlotChunk = 64;
 constexpr int kSlotILP = 8;
 
 // One element per thread: its d table values stay in registers and are reused by every
-// candidate of the batch; kSlotILP candidates are processed together so their k-sums and
-// exps interleave. MAXD is a compile-time bound on d (dispatch below), so the k loop is
-// fully unrolled with no dead iterations.
+// candidate of the batch; kSlotILP candidates are processed together, branch-free (exp_neg,
+// stores predicated), so their k-sums and exps interleave. MAXD is a compile-time bound on d
+// (dispatch below), so the k loop is fully unrolled with no dead iterations.
 template <int MAXD>
 __global__ void __launch_bounds__(256) assemble_kernel(
     const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
@@ -83,6 +84,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     int* __restrict__ status) {
   __shared__ double th[kAsmSlotChunk * MAXD];
   __shared__ int sl[kAsmSlotChunk];
+  __shared__ long long soff[kAsmSlotChunk];
   const int tile = blockIdx.x;
   int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
   while ((I + 1) * (I + 2) / 2 <= tile) ++I;
@@ -90,36 +92,43 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   const int J = tile - I * (I + 1) / 2;
   const double* tb = table + (size_t)tile * d * TILE_ELEMS;
   const double diag_base = __dadd_rn(1.0, nugget);  // correlation.hpp:193
+  double* const fbase = factors + (size_t)tile * TILE_ELEMS;
 
   for (int c0 = 0; c0 < nslots; c0 += kAsmSlotChunk) {
     const int cn = min(kAsmSlotChunk, nslots - c0);
     __syncthreads();
+    // Entries past cn replicate the last live slot (same theta -> the same value rewritten
+    // to the same address), so the kSlotILP groups below need no per-slot guard.
     for (int q = threadIdx.x; q < kAsmSlotChunk * MAXD; q += blockDim.x) {
       const int si = q / MAXD, k = q - si * MAXD;
-      th[q] = (si < cn && k < d) ? theta[(size_t)slots[c0 + si] * d + k] : 0.0;
+      th[q] = k < d ? theta[(size_t)slots[c0 + min(si, cn - 1)] * d + k] : 0.0;
     }
-    for (int q = threadIdx.x; q < cn; q += blockDim.x) sl[q] = slots[c0 + q];
+    for (int q = threadIdx.x; q < kAsmSlotChunk; q += blockDim.x) {
+      const int slot = slots[c0 + min(q, cn - 1)];
+      sl[q] = slot;
+      soff[q] = (long long)slot * (long long)slot_stride;
+    }
     __syncthreads();
+    const int cn_pad = (cn + kSlotILP - 1) / kSlotILP * kSlotILP;
     for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS;
          e += gridDim.y * blockDim.x) {
       int r, c;
       elem_rc(e, r, c);
       const int i = I * TILE + r, j = J * TILE + c;
       const bool pad = i >= n || j >= n;
-      double* dst = factors + (size_t)tile * TILE_ELEMS + e;
+      double* dst = fbase + e;
       if (pad || i == j) {
         for (int si = 0; si < cn; ++si) {
           const int slot = sl[si];
-          dst[(size_t)slot * slot_stride] =
-              pad ? (i == j ? 1.0 : 0.0) : __dadd_rn(diag_base, jitter[slot]);  // backend.hpp:107-109
+          dst[soff[si]] = pad ? (i == j ? 1.0 : 0.0) : __dadd_rn(diag_base, jitter[slot]);  // backend.hpp:107-109
         }
         continue;
       }
       double t[MAXD];
 #pragma unroll
       for (int k = 0; k < MAXD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
-      for (int s0 = 0; s0 < cn; s0 += kSlotILP) {
-        double s[kSlotILP];
+      for (int s0 = 0; s0 < cn_pad; s0 += kSlotILP) {
+        double s[kSlotILP], v[kSlotILP];
 #pragma unroll
         for (int q = 0; q < kSlotILP; ++q) s[q] = 0.0;
 #pragma unroll
@@ -128,13 +137,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(
           for (int q = 0; q < kSlotILP; ++q) s[q] = fma(th[(s0 + q) * MAXD + k], t[k], s[q]);
         }
 #pragma unroll
+        for (int q = 0; q < kSlotILP; ++q) v[q] = exp_neg(s[q]);
+#pragma unroll
         for (int q = 0; q < kSlotILP; ++q) {
-          if (s0 + q < cn) {
-            const int slot = sl[s0 + q];
-            const double v = exp(-s[q]);
-            if (!isfinite(v)) status[slot] = 2;  // GPEMU_SLOT_NONFINITE
-            dst[(size_t)slot * slot_stride] = v;
-          }
+          dst[soff[s0 + q]] = v[q];
+          if (!isfinite(v[q]) || isnan(s[q])) status[sl[s0 + q]] = 2;  // GPEMU_SLOT_NONFINITE (correlation.hpp:58-61)
         }
       }
     }
@@ -191,8 +198,8 @@ __global__ void build_corr_rowmajor_kernel(const double* __restrict__ X, int n, 
       const double term = pow_abs(X[(size_t)i * d + k] - X[(size_t)j * d + k], p);
       s = __dadd_rn(s, __dmul_rn(theta[k], term));
     }
-    const double v = exp(-s);
-    if (!isfinite(v)) *bad = 1;
+    const double v = exp_neg(s);
+    if (!isfinite(v) || isnan(s)) *bad = 1;
     R[(size_t)i * n + j] = v;
     R[(size_t)j * n + i] = v;
   }
@@ -216,8 +223,8 @@ __global__ void corr_vectors_kernel(const double* __restrict__ Xt, int N,
       const double term = pow_abs(Xt[(size_t)j * d + k] - X[(size_t)i * d + k], p);
       s = __dadd_rn(s, __dmul_rn(theta[k], term));
     }
-    const double v = exp(-s);
-    if (!isfinite(v)) *bad = 1;
+    const double v = exp_neg(s);
+    if (!isfinite(v) || isnan(s)) *bad = 1;
     r[(size_t)j * n + i] = v;
   }
 }
