@@ -1167,16 +1167,17 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   if (N == 0) return GPEMU_OK;
   ck(cudaSetDevice(m->ctx->device), "cudaSetDevice");
   cudaStream_t s = m->ctx->stream;
-  DevBuf<double> dXt, dy, dm;
+  DevBuf<double> dXt, dy, dm, dpart;
   DevBuf<int> bad;
   dXt.alloc(N * m->d);
   dy.alloc(N);
+  dpart.alloc((size_t)predict_blocks(m->n) * N);
   bad.alloc(1);
   ck(cudaMemcpyAsync(dXt.p, Xtest, N * m->d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D Xtest");
   ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
-  launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p, dy.p,
-                 bad.p, s);
-  m->ctx->launches += 1;
+  launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
+                 dpart.p, dy.p, bad.p, s);
+  m->ctx->launches += 2;
   if (mse) {
     // W = L^-1 r for chunks of test points as extension rows of the factor (DMMA tiles),
     // then one warp per point: the kriging MSE (and yhat from w, which is not used here:

@@ -69,8 +69,10 @@ void launch_tri_solve(const double* tiles, int n, int NT, const double* b, doubl
 // ---- K4: prediction (kernels_predict.cu) -----------------------------------
 // yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50); when mse is
 // non-null also w = L^-1 r_j and the kriging MSE.
+int predict_blocks(int n);
+// part: predict_blocks(n) * N doubles of scratch
 void launch_predict(const double* Xt, int N, const double* X, int n, int d, const double* theta,
-                    double p, double mu, const double* alpha, double* yhat, int* bad,
+                    double p, double mu, const double* alpha, double* part, double* yhat, int* bad,
                     cudaStream_t s);
 void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
                         const double* theta, double p, double sigma2, const double* tiles, int NT,

@@ -20,11 +20,7 @@
 namespace gpemu_dev {
 
 
-__device__ __forceinline__ double pow_abs(double delta, double p) {
-  if (delta == 0.0) return 0.0;
-  const double a = delta < 0.0 ? -delta : delta;
-  return exp(__dmul_rn(p, log(a)));
-}
+__device__ __forceinline__ double pow_abs(double delta, double p) { return pow_abs_fast(delta, p); }
 
 // Table: [tile][k][elem], tile-major over the packed lower tiles.
 __global__ void pow_table_kernel(const double* __restrict__ X, int n, int d, double p, int NT,

@@ -12,94 +12,106 @@
 // a fixed-order block reduction finishes each dot (deterministic).
 #include <cuda_runtime.h>
 
+#include "fastmath.cuh"
 #include "kernels.h"
 #include "layout.cuh"
 
 namespace gpemu_dev {
 
-constexpr int kPts = 16;
-constexpr int kTrainChunk = 256;
+constexpr int kPredThreads = 128;
+constexpr int kTrainBlock = 1024;  // training rows per partial dot (fixed: bits independent of N)
+constexpr int kTrainStage = 128;   // rows staged in shared memory at a time
 
-__device__ __forceinline__ double pow_abs_p(double delta, double p) {
-  if (delta == 0.0) return 0.0;
-  const double a = delta < 0.0 ? -delta : delta;
-  return exp(__dmul_rn(p, log(a)));
-}
+__device__ __forceinline__ double pow_abs_p(double delta, double p) { return pow_abs_fast(delta, p); }
 
-__global__ void __launch_bounds__(256) predict_kernel(const double* __restrict__ Xt, int N,
-                                                      const double* __restrict__ X, int n, int d,
-                                                      const double* __restrict__ theta, double p,
-                                                      double mu, const double* __restrict__ alpha,
-                                                      double* __restrict__ yhat, int* bad) {
-  extern __shared__ double dyn[];
-  double* xs = dyn;                          // [kTrainChunk][d]
-  double* as = xs + kTrainChunk * d;         // [kTrainChunk]
-  double* ts = as + kTrainChunk;             // [kPts][d]
-  double* th = ts + kPts * d;                // [d]
-  __shared__ double red[kPts][256 / 32];
-  const int j0 = blockIdx.x * kPts;
-  const int np = min(kPts, N - j0);
-  for (int q = threadIdx.x; q < kPts * d; q += blockDim.x) {
-    const int pj = q / d, k = q - pj * d;
-    ts[pj * d + k] = pj < np ? Xt[(size_t)(j0 + pj) * d + k] : 0.0;
+// yhat_j = mu + sum_i r_i(x_j) alpha_i (predictor.hpp:36-44): one thread per test point,
+// ascending i as dot_accumulate (matrix.hpp:64-69). Training rows are split into fixed
+// kTrainBlock blocks (blockIdx.y); each block's partial dot goes to part[blk][j] and
+// predict_combine adds them in block order (deterministic, independent of N). Staged
+// training rows are read by every thread at the same address (shared-memory broadcast);
+// MAXD unrolls the d pow terms so they interleave (fastmath.cuh is branch-free).
+template <int MAXD>
+__global__ void __launch_bounds__(kPredThreads) predict_kernel(
+    const double* __restrict__ Xt, int N, const double* __restrict__ X, int n, int d,
+    const double* __restrict__ theta, double p, const double* __restrict__ alpha,
+    double* __restrict__ part, int* bad) {
+  __shared__ double xs[kTrainStage][MAXD];
+  __shared__ double as[kTrainStage];
+  const int j = blockIdx.x * kPredThreads + threadIdx.x;
+  const int jc = min(j, N - 1);
+  double xt[MAXD], th[MAXD];
+#pragma unroll
+  for (int k = 0; k < MAXD; ++k) {
+    xt[k] = k < d ? Xt[(size_t)jc * d + k] : 0.0;
+    th[k] = k < d ? theta[k] : 0.0;  // zero terms leave the sequential sum unchanged
   }
-  for (int k = threadIdx.x; k < d; k += blockDim.x) th[k] = theta[k];
-  double acc[kPts];
-#pragma unroll
-  for (int pj = 0; pj < kPts; ++pj) acc[pj] = 0.0;
-  for (int c0 = 0; c0 < n; c0 += kTrainChunk) {
-    const int cn = min(kTrainChunk, n - c0);
+  const int i0 = blockIdx.y * kTrainBlock, i1 = min(n, i0 + kTrainBlock);
+  double acc = 0.0;
+  bool nonfinite = false;
+  for (int c0 = i0; c0 < i1; c0 += kTrainStage) {
+    const int cn = min(kTrainStage, i1 - c0);
     __syncthreads();
-    for (int q = threadIdx.x; q < cn * d; q += blockDim.x) {
-      const int i = q / d, k = q - i * d;
-      xs[i * d + k] = X[(size_t)(c0 + i) * d + k];
+    for (int q = threadIdx.x; q < kTrainStage * MAXD; q += kPredThreads) {
+      const int r = q / MAXD, k = q - r * MAXD;
+      xs[r][k] = (r < cn && k < d) ? X[(size_t)(c0 + r) * d + k] : 0.0;
     }
-    for (int q = threadIdx.x; q < cn; q += blockDim.x) as[q] = alpha[c0 + q];
+    for (int q = threadIdx.x; q < kTrainStage; q += kPredThreads) as[q] = q < cn ? alpha[c0 + q] : 0.0;
     __syncthreads();
-    const int i = threadIdx.x;
-    if (i < cn) {
-      const double ai = as[i];
+    for (int r = 0; r < cn; ++r) {
+      double s = 0.0;
 #pragma unroll
-      for (int pj = 0; pj < kPts; ++pj) {
-        if (pj < np) {
-          double s = 0.0;
-          for (int k = 0; k < d; ++k) {
-            const double term = pow_abs_p(ts[pj * d + k] - xs[i * d + k], p);
-            s = __dadd_rn(s, __dmul_rn(th[k], term));
-          }
-          const double r = exp(-s);
-          if (!isfinite(r)) *bad = 1;
-          acc[pj] = fma(r, ai, acc[pj]);
-        }
-      }
+      for (int k = 0; k < MAXD; ++k) s = __dadd_rn(s, __dmul_rn(th[k], pow_abs_p(xt[k] - xs[r][k], p)));
+      const double v = exp_neg(s);
+      nonfinite |= !isfinite(v) || isnan(s);
+      acc = fma(v, as[r], acc);
     }
   }
-  // deterministic block reduction: warp shuffle tree, then warps in order
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int pj = 0; pj < kPts; ++pj) {
-    double v = acc[pj];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-    if (lane == 0) red[pj][warp] = v;
-  }
-  __syncthreads();
-  if (threadIdx.x < np) {
-    double s = 0.0;
-    for (int w = 0; w < 256 / 32; ++w) s += red[threadIdx.x][w];
-    yhat[j0 + threadIdx.x] = mu + s;
+  if (j < N) {
+    part[(size_t)blockIdx.y * N + j] = acc;
+    if (nonfinite) *bad = 1;
   }
 }
 
+__global__ void predict_combine_kernel(const double* __restrict__ part, int N, int nblk, double mu,
+                                       double* __restrict__ yhat) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  double s = part[j];
+  for (int b = 1; b < nblk; ++b) s += part[(size_t)b * N + j];
+  yhat[j] = mu + s;
+}
+
+int predict_blocks(int n) { return (n + kTrainBlock - 1) / kTrainBlock; }
+
+template <int MAXD>
+static void launch_pred(dim3 grid, cudaStream_t s, const double* Xt, int N, const double* X, int n,
+                        int d, const double* theta, double p, const double* alpha, double* part,
+                        int* bad) {
+  predict_kernel<MAXD><<<grid, kPredThreads, 0, s>>>(Xt, N, X, n, d, theta, p, alpha, part, bad);
+}
+
+// part: predict_blocks(n) * N doubles of scratch.
 void launch_predict(const double* Xt, int N, const double* X, int n, int d, const double* theta,
-                    double p, double mu, const double* alpha, double* yhat, int* bad,
+                    double p, double mu, const double* alpha, double* part, double* yhat, int* bad,
                     cudaStream_t s) {
   if (N <= 0) return;
-  const size_t smem = ((size_t)kTrainChunk * d + kTrainChunk + (size_t)kPts * d + d) * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(predict_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  predict_kernel<<<(N + kPts - 1) / kPts, 256, smem, s>>>(Xt, N, X, n, d, theta, p, mu, alpha,
-                                                          yhat, bad);
+  const int nblk = predict_blocks(n);
+  const dim3 grid((N + kPredThreads - 1) / kPredThreads, nblk);
+#define GPEMU_PRED(D) launch_pred<D>(grid, s, Xt, N, X, n, d, theta, p, alpha, part, bad)
+  if (d <= 1) GPEMU_PRED(1);
+  else if (d <= 2) GPEMU_PRED(2);
+  else if (d <= 3) GPEMU_PRED(3);
+  else if (d <= 4) GPEMU_PRED(4);
+  else if (d <= 6) GPEMU_PRED(6);
+  else if (d <= 8) GPEMU_PRED(8);
+  else if (d <= 10) GPEMU_PRED(10);
+  else if (d <= 12) GPEMU_PRED(12);
+  else if (d <= 16) GPEMU_PRED(16);
+  else if (d <= 20) GPEMU_PRED(20);
+  else if (d <= 24) GPEMU_PRED(24);
+  else GPEMU_PRED(32);
+#undef GPEMU_PRED
+  predict_combine_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, N, nblk, mu, yhat);
 }
 
 // MSE, one CTA per test point: r into shared memory, column-oriented forward
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(512) mse_point_kernel(const double* __restrict
       const double term = pow_abs_p(Xt[(size_t)j * d + k] - X[(size_t)i * d + k], p);
       s = __dadd_rn(s, __dmul_rn(theta[k], term));
     }
-    const double r = exp(-s);
+    const double r = exp_neg(s);
     if (!isfinite(r)) *bad = 1;
     w[i] = r;
   }
@@ -185,49 +197,73 @@ namespace gpemu_dev {
 // (the same OFF-task path as the factorization), then one warp per point reduces its row.
 
 // Cross-correlation tile (It, J): rows = test points It*128 + r, cols = design points
-// J*128 + c; corr_vector arithmetic (correlation.hpp:84-87): sequential k, no FMA.
+// J*128 + c; corr_vector arithmetic (correlation.hpp:84-87): sequential k, no FMA. Design
+// coordinates are staged [k][c] (consecutive c across a warp: conflict-free), test
+// coordinates [r][k] (one r per warp row: broadcast); padding rows/cols are computed on
+// clamped coordinates and written as 0, so the MAXD-unrolled body has no branches.
+template <int MAXD>
 __global__ void __launch_bounds__(256) cross_tiles_kernel(const double* __restrict__ Xt, int N,
                                                           const double* __restrict__ X, int n,
                                                           int d, const double* __restrict__ theta,
                                                           double p, int NT,
                                                           double* __restrict__ ext, int* bad) {
-  extern __shared__ double sm[];
-  double* xt = sm;                 // [128][d]
-  double* xs = xt + TILE * d;      // [128][d]
-  double* th = xs + TILE * d;      // [d]
+  extern __shared__ double cross_sm[];  // xt[TILE][MAXD], xs[MAXD][TILE], th[MAXD]
+  double(*xt)[MAXD] = reinterpret_cast<double(*)[MAXD]>(cross_sm);
+  double(*xs)[TILE] = reinterpret_cast<double(*)[TILE]>(cross_sm + TILE * MAXD);
+  double* th = cross_sm + 2 * TILE * MAXD;
   const int tile = blockIdx.x;
   const int It = tile / NT, J = tile - It * NT;
-  for (int q = threadIdx.x; q < TILE * d; q += blockDim.x) {
-    const int r = q / d, k = q - r * d;
-    const int pt = It * TILE + r, pi = J * TILE + r;
-    xt[q] = pt < N ? Xt[(size_t)pt * d + k] : 0.0;
-    xs[q] = pi < n ? X[(size_t)pi * d + k] : 0.0;
+  for (int q = threadIdx.x; q < TILE * MAXD; q += blockDim.x) {
+    const int r = q / MAXD, k = q - r * MAXD;
+    const int pt = min(It * TILE + r, N - 1), pi = min(J * TILE + r, n - 1);
+    xt[r][k] = k < d ? Xt[(size_t)pt * d + k] : 0.0;
+    xs[k][r] = k < d ? X[(size_t)pi * d + k] : 0.0;
   }
-  for (int k = threadIdx.x; k < d; k += blockDim.x) th[k] = theta[k];
+  for (int k = threadIdx.x; k < MAXD; k += blockDim.x) th[k] = k < d ? theta[k] : 0.0;
   __syncthreads();
   double* out = ext + (size_t)tile * TILE_ELEMS;
+  bool nonfinite = false;
   for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
     int r, c;
     elem_rc(e, r, c);
-    double v = 0.0;
-    if (It * TILE + r < N && J * TILE + c < n) {
-      double s = 0.0;
-      for (int k = 0; k < d; ++k)
-        s = __dadd_rn(s, __dmul_rn(th[k], pow_abs_p(xt[r * d + k] - xs[c * d + k], p)));
-      v = exp(-s);
-      if (!isfinite(v)) *bad = 1;
-    }
-    out[e] = v;
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < MAXD; ++k) s = __dadd_rn(s, __dmul_rn(th[k], pow_abs_p(xt[r][k] - xs[k][c], p)));
+    const double v = exp_neg(s);
+    const bool live = It * TILE + r < N && J * TILE + c < n;
+    nonfinite |= live && (!isfinite(v) || isnan(s));
+    out[e] = live ? v : 0.0;
   }
+  if (nonfinite) *bad = 1;
+}
+
+template <int MAXD>
+static void launch_cross(dim3 grid, cudaStream_t s, const double* Xt, int N, const double* X, int n,
+                         int d, const double* theta, double p, int NT, double* ext, int* bad) {
+  const int smem = (2 * TILE * MAXD + MAXD) * (int)sizeof(double);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(cross_tiles_kernel<MAXD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cross_tiles_kernel<MAXD><<<grid, 256, smem, s>>>(Xt, N, X, n, d, theta, p, NT, ext, bad);
 }
 
 void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,
                         const double* theta, double p, int NT, int RT, double* ext, int* bad,
                         cudaStream_t s) {
-  const size_t smem = (2 * (size_t)TILE * d + d) * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(cross_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cross_tiles_kernel<<<dim3(RT * NT, 4), 256, smem, s>>>(Xt, N, X, n, d, theta, p, NT, ext, bad);
+  const dim3 grid(RT * NT, 4);
+#define GPEMU_CROSS(D) launch_cross<D>(grid, s, Xt, N, X, n, d, theta, p, NT, ext, bad)
+  if (d <= 1) GPEMU_CROSS(1);
+  else if (d <= 2) GPEMU_CROSS(2);
+  else if (d <= 3) GPEMU_CROSS(3);
+  else if (d <= 4) GPEMU_CROSS(4);
+  else if (d <= 6) GPEMU_CROSS(6);
+  else if (d <= 8) GPEMU_CROSS(8);
+  else if (d <= 10) GPEMU_CROSS(10);
+  else if (d <= 12) GPEMU_CROSS(12);
+  else if (d <= 16) GPEMU_CROSS(16);
+  else if (d <= 20) GPEMU_CROSS(20);
+  else if (d <= 24) GPEMU_CROSS(24);
+  else GPEMU_CROSS(32);
+#undef GPEMU_CROSS
 }
 
 // One warp per test point: fixed-order lane partials + shuffle tree (deterministic).
