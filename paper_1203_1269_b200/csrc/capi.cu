@@ -65,6 +65,9 @@ struct DevBuf {
     ck(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
     count = c;
   }
+  void reserve(size_t c) {  // grow-only: keeps the allocation when it is large enough
+    if (count < c) alloc(c);
+  }
   void free() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -189,6 +192,9 @@ struct gpemu_model {
   DevBuf<double> ext;
   DevBuf<int> ext_flags, ext_slot, counter, error;
   int ext_rt_cap = 0, epoch = 0;
+  // predict scratch, grown on demand and reused across calls (no per-call cudaMalloc/Free)
+  DevBuf<double> pred_xt, pred_y, pred_mse, pred_part;
+  DevBuf<int> pred_bad;
 };
 
 namespace {
@@ -1167,22 +1173,24 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   if (N == 0) return GPEMU_OK;
   ck(cudaSetDevice(m->ctx->device), "cudaSetDevice");
   cudaStream_t s = m->ctx->stream;
-  DevBuf<double> dXt, dy, dm, dpart;
-  DevBuf<int> bad;
-  dXt.alloc(N * m->d);
-  dy.alloc(N);
-  dpart.alloc((size_t)predict_blocks(m->n) * N);
-  bad.alloc(1);
+  DevBuf<double>&dXt = m->pred_xt, &dy = m->pred_y, &dm = m->pred_mse, &dpart = m->pred_part;
+  DevBuf<int>& bad = m->pred_bad;
+  dXt.reserve(N * m->d);
+  dy.reserve(N);
+  dpart.reserve((size_t)predict_blocks(m->n) * N);
+  bad.reserve(1);
   ck(cudaMemcpyAsync(dXt.p, Xtest, N * m->d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D Xtest");
   ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
-  launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
-                 dpart.p, dy.p, bad.p, s);
-  m->ctx->launches += 2;
-  if (mse) {
-    // W = L^-1 r for chunks of test points as extension rows of the factor (DMMA tiles),
-    // then one warp per point: the kriging MSE (and yhat from w, which is not used here:
-    // yhat keeps the reference's r.alpha route above).
-    dm.alloc(N);
+  if (!mse) {
+    launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
+                   dpart.p, dy.p, bad.p, s);
+    m->ctx->launches += 2;
+  } else {
+    // Cross-correlation tiles r for chunks of test points; yhat = mu + r.alpha from the tiles
+    // (predict_kernel's summation order: the same bits as the yhat-only call); then
+    // W = L^-1 r as extension rows of the factor (DMMA tiles) and one warp per point: the
+    // kriging MSE.
+    dm.reserve(N);
     const int NT = m->NT;
     const int chunk_pts = 65536;
     const int rt_cap = (int)std::min<size_t>((N + TILE - 1) / TILE, chunk_pts / TILE);
@@ -1202,6 +1210,7 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
       const int RT = (Nc + TILE - 1) / TILE;
       launch_cross_tiles(dXt.p + p0 * m->d, Nc, m->X.p, m->n, m->d, m->theta_d.p, m->p, NT, RT,
                          m->ext.p, bad.p, s);
+      launch_yhat_tiles(m->ext.p, Nc, m->n, NT, m->alpha.p, dpart.p, N, p0, s);
       DagLaunch a;
       a.factors = m->tiles.p;
       a.borders = nullptr;
@@ -1221,8 +1230,10 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
       launch_chol_dag(a, m->ctx->num_sms, s);
       launch_ext_reduce(m->ext.p, Nc, m->n, NT, m->u.p, m->v.p, m->mu, m->sigma2, m->vtv,
                         nullptr, dm.p + p0, s);
-      m->ctx->launches += 3;
+      m->ctx->launches += 4;
     }
+    launch_predict_combine(dpart.p, (int)N, m->n, m->mu, dy.p, s);
+    m->ctx->launches += 1;
   }
   ck(cudaGetLastError(), "predict launch");
   int hbad = 0;

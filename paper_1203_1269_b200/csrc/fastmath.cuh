@@ -38,8 +38,10 @@ constexpr double kLn2Lo = 1.90821492927058770002e-10;
 //   r_lo = -k ln2_lo; e^r = (1 + r_hi) [Fast2Sum] + (r^2 P(r) + r_lo);
 //   result = (e^r 2^(k>>1)) 2^(k - (k>>1)): both scale factors are normal, so subnormal
 //   results are rounded once.
-__device__ __forceinline__ double exp_neg(double s) {
-  const double x = fmin(fmax(-s, -1000.0), 1000.0);
+template <bool kClampHigh>
+__device__ __forceinline__ double exp_core(double x) {
+  x = fmax(x, -1000.0);
+  if (kClampHigh) x = fmin(x, 1000.0);
   const double kd = fma(x, 1.4426950408889634, 6755399441055744.0);  // 1.5 * 2^52: rint
   const int k = __double2loint(kd);
   const double kf = kd - 6755399441055744.0;
@@ -57,17 +59,20 @@ __device__ __forceinline__ double exp_neg(double s) {
   return (e * __hiloint2double((k1 + 1023) << 20, 0)) * __hiloint2double((k2 + 1023) << 20, 0);
 }
 
-__device__ __forceinline__ double two_sum(double a, double b, double& err) {
+__device__ __forceinline__ double exp_neg(double s) { return exp_core<true>(-s); }
+
+// Fast2Sum: s + err == a + b exactly when |a| >= |b| (or a == 0).
+__device__ __forceinline__ double fast_two_sum(double a, double b, double& err) {
   const double s = __dadd_rn(a, b);
-  const double bb = __dsub_rn(s, a);
-  err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  err = __dsub_rn(b, __dsub_rn(s, a));
   return s;
 }
 
 // log(a) for finite a > 0 (subnormals included): fdlibm e_log.c reduction and minimax
 // coefficients Lg1..Lg7, a = 2^k m, m in [sqrt(2)/2, sqrt(2)), f = m - 1, s = f / (2 + f),
 // log m = (f - f^2/2) + (s (f^2/2 + R(s^2)) - lo(f^2/2)); f - f^2/2 and k ln2_hi + (f - f^2/2)
-// are exact two-sums so only the last addition rounds. The division is an rcp.approx seed +
+// are exact Fast2Sums (|f^2/2| <= 0.21 |f|; |k ln2_hi| >= 0.69 > |log m| or k = 0) so only
+// the last addition rounds. The division is an rcp.approx seed +
 // two FMA Newton steps (2 + f lies in [1.29, 2.42]: no special cases).
 __device__ __forceinline__ double log_pos(double a) {
   const bool sub = a < 2.2250738585072014e-308;
@@ -96,16 +101,18 @@ __device__ __forceinline__ double log_pos(double a) {
                                      6.666666666666735130e-01));
   const double c = fma(s, __dadd_rn(hfsq, __dadd_rn(t2, t1)), -hfsq_lo);
   double dl, rl;
-  const double dh = two_sum(f, -hfsq, dl);
+  const double dh = fast_two_sum(f, -hfsq, dl);
   const double dk = (double)k;
-  const double rh = two_sum(__dmul_rn(dk, kLn2Hi), dh, rl);
+  const double rh = fast_two_sum(__dmul_rn(dk, kLn2Hi), dh, rl);
   return __dadd_rn(rh, __dadd_rn(rl, __dadd_rn(dl, fma(dk, kLn2Lo, c))));
 }
 
 // detail::pow_abs (correlation.hpp:29-34): |delta|^p = exp(p log|delta|), 0 -> 0, branch-free.
 __device__ __forceinline__ double pow_abs_fast(double delta, double p) {
+  // p log a <= p log(1 + 2e-12): no upper clamp needed; log_pos(0) is finite (-746.5, via the
+  // subnormal path) and its result is discarded by the select.
   const double a = fabs(delta);
-  const double v = exp_neg(-__dmul_rn(p, log_pos(a == 0.0 ? 1.0 : a)));
+  const double v = exp_core<false>(__dmul_rn(p, log_pos(a)));
   return a == 0.0 ? 0.0 : v;
 }
 

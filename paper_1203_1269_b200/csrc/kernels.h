@@ -70,6 +70,11 @@ void launch_tri_solve(const double* tiles, int n, int NT, const double* b, doubl
 // yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50); when mse is
 // non-null also w = L^-1 r_j and the kriging MSE.
 int predict_blocks(int n);
+// yhat partials from a chunk's cross tiles (before the extension DAG), same order as predict
+void launch_yhat_tiles(const double* ext, int Nc, int n, int NT, const double* alpha, double* part,
+                       size_t N, size_t p0, cudaStream_t s);
+void launch_predict_combine(const double* part, int N, int n, double mu, double* yhat,
+                            cudaStream_t s);
 // part: predict_blocks(n) * N doubles of scratch
 void launch_predict(const double* Xt, int N, const double* X, int n, int d, const double* theta,
                     double p, double mu, const double* alpha, double* part, double* yhat, int* bad,

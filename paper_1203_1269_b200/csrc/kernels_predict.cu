@@ -25,13 +25,14 @@ constexpr int kTrainStage = 128;   // rows staged in shared memory at a time
 __device__ __forceinline__ double pow_abs_p(double delta, double p) { return pow_abs_fast(delta, p); }
 
 // yhat_j = mu + sum_i r_i(x_j) alpha_i (predictor.hpp:36-44): one thread per test point,
-// ascending i as dot_accumulate (matrix.hpp:64-69). Training rows are split into fixed
-// kTrainBlock blocks (blockIdx.y); each block's partial dot goes to part[blk][j] and
-// predict_combine adds them in block order (deterministic, independent of N). Staged
+// ascending i (dot_accumulate, matrix.hpp:64-69) inside each 128-row tile; tile partials are
+// added in order inside fixed kTrainBlock blocks (blockIdx.y), each block's partial goes to
+// part[blk][j] and predict_combine adds them in block order. The order is independent of N
+// and identical to yhat_tiles_kernel's (the MSE path), so yhat is the same bits either way. Staged
 // training rows are read by every thread at the same address (shared-memory broadcast);
 // MAXD unrolls the d pow terms so they interleave (fastmath.cuh is branch-free).
 template <int MAXD>
-__global__ void __launch_bounds__(kPredThreads) predict_kernel(
+__global__ void __launch_bounds__(kPredThreads, MAXD <= 12 ? 6 : 4) predict_kernel(
     const double* __restrict__ Xt, int N, const double* __restrict__ X, int n, int d,
     const double* __restrict__ theta, double p, const double* __restrict__ alpha,
     double* __restrict__ part, int* bad) {
@@ -57,14 +58,16 @@ __global__ void __launch_bounds__(kPredThreads) predict_kernel(
     }
     for (int q = threadIdx.x; q < kTrainStage; q += kPredThreads) as[q] = q < cn ? alpha[c0 + q] : 0.0;
     __syncthreads();
+    double tacc = 0.0;  // this 128-row tile's partial (yhat_tiles_kernel uses the same order)
     for (int r = 0; r < cn; ++r) {
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < MAXD; ++k) s = __dadd_rn(s, __dmul_rn(th[k], pow_abs_p(xt[k] - xs[r][k], p)));
       const double v = exp_neg(s);
       nonfinite |= !isfinite(v) || isnan(s);
-      acc = fma(v, as[r], acc);
+      tacc = fma(v, as[r], tacc);
     }
+    acc = __dadd_rn(acc, tacc);
   }
   if (j < N) {
     part[(size_t)blockIdx.y * N + j] = acc;
@@ -264,6 +267,53 @@ void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,
   else if (d <= 24) GPEMU_CROSS(24);
   else GPEMU_CROSS(32);
 #undef GPEMU_CROSS
+}
+
+// yhat from the cross-correlation tiles of one chunk (before the extension DAG overwrites
+// them with W = L^-1 r): CTA (It, blk) owns 128 test points and the kTrainBlock/128 tiles
+// of training block blk; each slab (128 x 32, contiguous) is staged through shared memory and
+// thread r walks its row in ascending column order -- predict_kernel's summation order.
+__global__ void __launch_bounds__(128) yhat_tiles_kernel(const double* __restrict__ ext, int Nc,
+                                                         int n, int NT,
+                                                         const double* __restrict__ alpha,
+                                                         double* __restrict__ part, size_t N,
+                                                         size_t p0) {
+  __shared__ double slab[SLAB_ELEMS];
+  __shared__ double al[SLAB];
+  const int It = blockIdx.x, blk = blockIdx.y;
+  const int r = threadIdx.x;
+  const int J0 = blk * (kTrainBlock / TILE), J1 = min(NT, J0 + kTrainBlock / TILE);
+  double acc = 0.0;
+  for (int J = J0; J < J1; ++J) {
+    const double* tl = ext + ((size_t)It * NT + J) * TILE_ELEMS;
+    double tacc = 0.0;
+    for (int sl = 0; sl < SLABS_PER_TILE; ++sl) {
+      const int cbase = J * TILE + sl * SLAB;
+      if (cbase >= n) break;  // all-padding slab: r = 0 there (same as predict_kernel's rows)
+      __syncthreads();
+      const double2* src = reinterpret_cast<const double2*>(tl + sl * SLAB_ELEMS);
+      double2* dst = reinterpret_cast<double2*>(slab);
+      for (int q = threadIdx.x; q < SLAB_ELEMS / 2; q += blockDim.x) dst[q] = src[q];
+      if (threadIdx.x < SLAB) al[threadIdx.x] = cbase + (int)threadIdx.x < n ? alpha[cbase + threadIdx.x] : 0.0;
+      __syncthreads();
+      const int cn = min(SLAB, n - cbase);
+      for (int cc = 0; cc < cn; ++cc) tacc = fma(slab[slab_off(r, cc)], al[cc], tacc);
+    }
+    acc = __dadd_rn(acc, tacc);
+  }
+  const int pt = It * TILE + r;
+  if (pt < Nc) part[(size_t)blk * N + p0 + pt] = acc;
+}
+
+void launch_yhat_tiles(const double* ext, int Nc, int n, int NT, const double* alpha, double* part,
+                       size_t N, size_t p0, cudaStream_t s) {
+  const dim3 grid((Nc + TILE - 1) / TILE, predict_blocks(n));
+  yhat_tiles_kernel<<<grid, TILE, 0, s>>>(ext, Nc, n, NT, alpha, part, N, p0);
+}
+
+void launch_predict_combine(const double* part, int N, int n, double mu, double* yhat,
+                            cudaStream_t s) {
+  predict_combine_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, N, predict_blocks(n), mu, yhat);
 }
 
 // One warp per test point: fixed-order lane partials + shuffle tree (deterministic).

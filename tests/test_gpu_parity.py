@@ -331,6 +331,16 @@ def test_mse_extension_rows_multi_tile(g, ctx, orc):
     alpha = orc.solve_upper(L, orc.solve_lower(L, y - ref["mu"][0]))
     yo = orc.predict(X, th, 1.95, ref["mu"][0], alpha, Xt)
     assert np.max(np.abs(yhat - yo)) <= 1e-8 * max(np.abs(yo).max(), np.abs(y).max())
+    # yhat from the cross tiles (MSE path) is the yhat-only kernel's value, bit for bit
+    assert np.array_equal(yhat, g.predict(m, Xt))
+    n2 = 1200  # two training blocks of 1024 rows, ragged last tile
+    X2 = rng.random((n2, d))
+    y2 = np.sin(3 * X2).sum(1)
+    m2 = g.model_at_theta(g.new_dataset(X2, y2), th, 1.95, 0.0, g.Backend(ctx))
+    Xt2 = rng.random((257, d))
+    yh2, _ = g.predict(m2, Xt2, with_mse=True)
+    assert np.array_equal(yh2, g.predict(m2, Xt2))
+    assert np.array_equal(g.predict(m2, Xt2[100:101]), yh2[100:101])  # independent of N
 
 
 @pytest.mark.parametrize("engine", ["simple", "dag"])

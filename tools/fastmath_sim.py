@@ -55,10 +55,9 @@ def exp_neg(s):
     return (e * 2.0 ** k1) * 2.0 ** (k - k1)
 
 
-def two_sum(a, b):
+def fast_two_sum(a, b):
     s = a + b
-    bb = s - a
-    return s, (a - (s - bb)) + (b - bb)
+    return s, b - (s - a)
 
 
 def log_pos(a):
@@ -84,9 +83,9 @@ def log_pos(a):
     t1 = w * fma(w, fma(w, LG[5], LG[3]), LG[1])
     t2 = z * fma(w, fma(w, fma(w, LG[6], LG[4]), LG[2]), LG[0])
     c = fma(s, hfsq + (t2 + t1), -hfsq_lo)
-    dh, dl = two_sum(f, -hfsq)
+    dh, dl = fast_two_sum(f, -hfsq)
     dk = float(k)
-    rh, rl = two_sum(dk * LN2_HI, dh)
+    rh, rl = fast_two_sum(dk * LN2_HI, dh)
     return rh + (rl + (dl + fma(dk, LN2_LO, c)))
 
 
