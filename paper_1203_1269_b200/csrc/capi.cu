@@ -199,6 +199,8 @@ struct gpemu_model {
 
 namespace {
 
+constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
+
 void run_chol(gpemu_plan* pl, int nact) {
   DagLaunch a;
   a.factors = pl->factors.p;
@@ -214,6 +216,10 @@ void run_chol(gpemu_plan* pl, int nact) {
   a.status = pl->status.p;
   a.error = pl->error.p;
   a.prof = pl->dag_prof.p;
+  if (a.prof) {
+    a.trace = a.prof + (size_t)pl->ctx->num_sms * 24 + 256;
+    a.trace_cap = kTraceTasks;
+  }
   if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
     launch_chol_simple(a, pl->ctx->stream);
   } else {
@@ -751,7 +757,7 @@ int gpemu_plan_phase_ms(gpemu_plan* pl, int phase, double* total_ms, int* launch
 int gpemu_plan_dag_profile(gpemu_plan* pl, int enable, uint64_t* out, size_t out_len) {
   GPEMU_GUARD_BEGIN
   if (!pl) return set_error(GPEMU_VALIDATION, "null plan");
-  const size_t len = (size_t)pl->ctx->num_sms * 24 + 256;
+  const size_t len = (size_t)pl->ctx->num_sms * 24 + 256 + (size_t)kTraceTasks * 4;
   if (out && pl->dag_prof.p) {
     ck(cudaStreamSynchronize(pl->ctx->stream), "dag_profile");
     ck(cudaMemcpy(out, pl->dag_prof.p, std::min(out_len, len) * sizeof(uint64_t), cudaMemcpyDeviceToHost),

@@ -44,7 +44,12 @@ struct DagLaunch {
   double* ext = nullptr;
   int ext_rt = 0;
   int* ext_flags = nullptr;  // [It][NT]
+  // optional per-task timeline (diagnostics): trace[ticket][4] = globaltimer ns at task start,
+  // after the GEMM phase, before the publish, and at the end; tickets >= trace_cap skipped
+  unsigned long long* trace = nullptr;
+  int trace_cap = 0;
 };
+
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s);
 void launch_chol_simple(const DagLaunch& a, cudaStream_t s);
 size_t chol_dag_smem_bytes();

@@ -132,7 +132,8 @@ struct Misc {
   int ticket;
   int skip;
   int fail;
-  int pad;
+  int bpos;
+  int I, j;
 };
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
@@ -304,26 +305,37 @@ __device__ __forceinline__ int p_off(int r, int c) {
   return r * 16 + ((((c >> 2) ^ (r & 3)) << 2) | (c & 3));
 }
 
+// Pivot root and reciprocal without the sqrt / DDIV call sequences: y ~ 1/sqrt(s) from
+// rsqrt.approx + two Newton steps (~1 ulp), d = s*y corrected once (Markstein: the correctly
+// rounded sqrt except in rare ties), r = y as the approximate reciprocal that div_by corrects
+// with one FMA residual. Evaluated redundantly by every lane from the broadcast pivot.
+__device__ __forceinline__ void pivot_root(double s, double& d, double& r) {
+  double y;
+  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(s));
+  const double hs = 0.5 * s;
+  y = fma(y, fma(-hs * y, y, 0.5), y);
+  y = fma(y, fma(-hs * y, y, 0.5), y);
+  const double d0 = s * y;
+  d = fma(fma(-d0, d0, s), 0.5 * y, d0);
+  r = y;
+}
+
 // In-register Cholesky of a 16x16 diagonal block, lane r (< 16) holding row r in xr.
 // Right-looking: column c is broadcast through colbuf. Pivot reciprocals -> rinv[0..15].
 // Returns false (uniform) on a failed pivot (backend.hpp:238).
 __device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* colbuf, double* rinv, int lane) {
+  bool ok = true;  // uniform: every lane sees the same pivots (no divergent exit in the loop)
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    double d = 0.0, r = 0.0;
-    int ok = 1;
+    double s = __shfl_sync(0xffffffffu, xr[c], c);
+    ok = ok && s > 0.0;
+    if (!ok) s = 1.0;  // keep the arithmetic finite after a failure; the block is discarded
+    double d, r;
+    pivot_root(s, d, r);
     if (lane == c) {
-      const double s = xr[c];
-      ok = s > 0.0;
-      d = ok ? sqrt(s) : 0.0;
-      r = ok ? 1.0 / d : 0.0;
       xr[c] = d;
-      if (ok) rinv[c] = r;
+      rinv[c] = r;
     }
-    d = __shfl_sync(0xffffffffu, d, c);
-    r = __shfl_sync(0xffffffffu, r, c);
-    ok = __shfl_sync(0xffffffffu, ok, c);
-    if (!ok) return false;
     if (lane > c && lane < 16) {
       xr[c] = div_by(xr[c], d, r);
       colbuf[lane] = xr[c];
@@ -336,7 +348,7 @@ __device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* colbuf, do
     }
     __syncwarp();
   }
-  return true;
+  return ok;
 }
 
 // C tile accessors in shared memory (tile layout).
@@ -474,27 +486,32 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     if (tid == 0) {
       const int t = atomicAdd(a.counter, 1);
       misc->ticket = t;
-      if (t < ntasks && !ext) {
-        int bpos, j, I;
-        decode_task(t, B, NT, bpos, j, I);
-        misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
-      } else {
-        misc->skip = 0;
-      }
+      misc->skip = 0;
       misc->fail = 0;
+      if (t < ntasks) {
+        int bpos = 0, j, I;
+        if (ext) {
+          j = t / a.ext_rt;
+          I = t - j * a.ext_rt;  // the extension row tile It
+        } else {
+          decode_task(t, B, NT, bpos, j, I);
+        }
+        misc->bpos = bpos;
+        misc->I = I;
+        misc->j = j;
+        if (!ext) misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
+      }
     }
     __syncthreads();
     const int t = misc->ticket;
     if (t >= ntasks) break;
     if (tid == 0) pr.lap(PR_TICKET);
-    int bpos, j, I, It = 0;
+    unsigned long long* trc = (a.trace && tid == 0 && t < a.trace_cap) ? a.trace + (size_t)t * 4 : nullptr;
+    if (trc) trc[0] = globaltimer_ns();
+    int bpos = misc->bpos, j = misc->j, I = misc->I, It = 0;
     if (ext) {
-      j = t / a.ext_rt;
-      It = t - j * a.ext_rt;
+      It = I;
       I = NT;  // below every factor row: never a DIAG task
-      bpos = 0;
-    } else {
-      decode_task(t, B, NT, bpos, j, I);
     }
     const bool diag = (I == j);
     const int slot = a.slots[bpos];
@@ -617,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       }
       consumer_sync();  // every consumer is done reading the stage ring
+      if (trc) trc[1] = globaltimer_ns();
       if (tid == 0) {
         pr.lap(PR_GEMM);
         pr.add(PR_SLABS, nslab);
@@ -649,6 +667,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
         }
         consumer_sync();
+        if (trc) trc[2] = globaltimer_ns();
         if (tid == 0) {
           publish_flag(&flags[j * NT + j], epoch);
           pr.lap(PR_DIAG_STORE);
@@ -751,6 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (tid == 0) pr.lap(PR_TRSM);
         }
         consumer_sync();
+        if (trc) trc[2] = globaltimer_ns();
         if (tid == 0) {
           publish_flag(ext ? &a.ext_flags[(size_t)It * NT + j] : &flags[I * NT + j], epoch);
           pr.lap(PR_OFF_STORE);
@@ -758,6 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       }
     }
     __syncthreads();
+    if (trc) trc[3] = globaltimer_ns();
     if (tid == 0) pr.lap(PR_TASK_END);
   }
   if (tid == 0) pr.add(PR_TOTAL, (unsigned long long)(clock64() - t_begin));

@@ -521,13 +521,15 @@ class ProfileEvaluator:
 
     def dag_profile(self, enable: bool = True, read: bool = False):
         """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""
-        out = np.zeros(148 * 24, dtype=np.uint64) if read else None
+        out = np.zeros(148 * 24 + 256 + 65536 * 4, dtype=np.uint64) if read else None
         _check(lib().gpemu_plan_dag_profile(self.handle, int(enable),
                                             None if out is None else out.ctypes.data, 0 if out is None else out.size))
         if out is None:
             return None
-        m = out.reshape(-1, 24)
-        return {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
+        m = out[:148 * 24].reshape(-1, 24)
+        res = {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
+        res["trace"] = out[148 * 24 + 256:].reshape(-1, 4)  # per ticket: start, gemm end, publish, end (ns)
+        return res
 
     def eval_batch_device(self, theta_ptr: int, B: int, out_ptr: int):
         """Device-resident batch: theta_ptr -> B x d doubles, out_ptr -> B x 8 records."""

@@ -11,7 +11,8 @@ nug = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
 rng = np.random.default_rng(0)
 X = rng.random((n, d))
 y = np.sin(3 * X).sum(1)
-ctx = g.Context(0, "dag")
+import os
+ctx = g.Context(0, os.environ.get("GPEMU_PROBE_ENGINE", "dag"))
 ev = g.ProfileEvaluator(g.new_dataset(X, y), p_exp, nug, g.Backend(ctx), max_batch=B)
 th = 10 ** rng.uniform(-1.0, 0.5, size=(B, d))
 dth = torch.from_numpy(th).cuda()
