@@ -72,8 +72,8 @@ void launch_tri_solve(const double* tiles, int n, int NT, const double* b, doubl
                       cudaStream_t s);
 
 // ---- K4: prediction (kernels_predict.cu) -----------------------------------
-// yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50); when mse is
-// non-null also w = L^-1 r_j and the kriging MSE.
+// yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50), in a fixed summation
+// order (128-row tiles inside 1024-row blocks) shared by the yhat-only and the MSE paths.
 int predict_blocks(int n);
 // yhat partials from a chunk's cross tiles (before the extension DAG), same order as predict
 void launch_yhat_tiles(const double* ext, int Nc, int n, int NT, const double* alpha, double* part,
@@ -84,10 +84,6 @@ void launch_predict_combine(const double* part, int N, int n, double mu, double*
 void launch_predict(const double* Xt, int N, const double* X, int n, int d, const double* theta,
                     double p, double mu, const double* alpha, double* part, double* yhat, int* bad,
                     cudaStream_t s);
-void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
-                        const double* theta, double p, double sigma2, const double* tiles, int NT,
-                        const double* v /* L^-1 1 */, double vtv, double* work /*N*Npad*/,
-                        double* mse, int* bad, cudaStream_t s);
 // Cross-correlation tiles of RT*128 test points against the design, [It][J] tile layout
 // (rows past N and columns past n are zero).
 void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,

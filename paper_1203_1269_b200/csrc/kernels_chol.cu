@@ -128,12 +128,15 @@ constexpr int kSmemBytes = kOffMisc + 64;
 constexpr long long kSpinLimitCycles = 20000000000LL;  // ~10 s: declare deadlock
 constexpr int kStageLd = 18;  // row stride (doubles) of the per-warp TRSM staging block
 
-struct Misc {
+struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's registers)
   int ticket;
   int skip;
   int fail;
   int bpos;
   int I, j;
+  unsigned ljj_phase;  // uses of ljj_bar (the OFF-task L(j,j) load)
+  int pad;
+  long long t_begin;   // PR_TOTAL start (profiling)
 };
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
@@ -478,9 +481,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   __syncthreads();
 
   uint32_t it = 0;  // slab iteration counter, advanced identically by both roles
-  uint32_t ljj_phase = 0;  // uses of ljj_bar (consumers)
+
   Prof pr{(a.prof && tid == 0) ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr, 0};
-  const long long t_begin = clock64();
+  if (tid == 0) {
+    misc->ljj_phase = 0;
+    misc->t_begin = clock64();
+  }
   pr.start();
   while (true) {
     if (tid == 0) {
@@ -506,8 +512,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
     const int t = misc->ticket;
     if (t >= ntasks) break;
     if (tid == 0) pr.lap(PR_TICKET);
-    unsigned long long* trc = (a.trace && tid == 0 && t < a.trace_cap) ? a.trace + (size_t)t * 4 : nullptr;
-    if (trc) trc[0] = globaltimer_ns();
+    // optional timeline stamps (diagnostics): the ticket is re-read from shared memory so no
+    // per-task pointer stays live across the mainloop
+    auto stamp = [&](int k) {
+      if (a.trace && tid == 0) {
+        const int tt = misc->ticket;
+        if (tt < a.trace_cap) a.trace[(size_t)tt * 4 + k] = globaltimer_ns();
+      }
+    };
+    stamp(0);
     int bpos = misc->bpos, j = misc->j, I = misc->I, It = 0;
     if (ext) {
       It = I;
@@ -634,7 +647,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       }
       consumer_sync();  // every consumer is done reading the stage ring
-      if (trc) trc[1] = globaltimer_ns();
+      stamp(1);
       if (tid == 0) {
         pr.lap(PR_GEMM);
         pr.add(PR_SLABS, nslab);
@@ -667,7 +680,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
         }
         consumer_sync();
-        if (trc) trc[2] = globaltimer_ns();
+        stamp(2);
         if (tid == 0) {
           publish_flag(&flags[j * NT + j], epoch);
           pr.lap(PR_DIAG_STORE);
@@ -705,8 +718,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
               bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, ljj_bar);
           }
-          mbar_wait(ljj_bar, ljj_phase & 1);
-          ++ljj_phase;
+          mbar_wait(ljj_bar, misc->ljj_phase & 1);
         }
         if (tid == 0) pr.lap(PR_OFF_WAIT);
         const bool run = !skip && (ext || *((volatile int*)&a.status[slot]) == 0);
@@ -770,18 +782,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (tid == 0) pr.lap(PR_TRSM);
         }
         consumer_sync();
-        if (trc) trc[2] = globaltimer_ns();
+        stamp(2);
         if (tid == 0) {
+          if (!skip) ++misc->ljj_phase;  // every consumer passed its ljj wait (consumer_sync above)
           publish_flag(ext ? &a.ext_flags[(size_t)It * NT + j] : &flags[I * NT + j], epoch);
           pr.lap(PR_OFF_STORE);
         }
       }
     }
     __syncthreads();
-    if (trc) trc[3] = globaltimer_ns();
+    stamp(3);
     if (tid == 0) pr.lap(PR_TASK_END);
   }
-  if (tid == 0) pr.add(PR_TOTAL, (unsigned long long)(clock64() - t_begin));
+  if (tid == 0) pr.add(PR_TOTAL, (unsigned long long)(clock64() - misc->t_begin));
 }
 }  // namespace
 

@@ -117,79 +117,6 @@ void launch_predict(const double* Xt, int N, const double* X, int n, int d, cons
   predict_combine_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, N, nblk, mu, yhat);
 }
 
-// MSE, one CTA per test point: r into shared memory, column-oriented forward
-// substitution w = L^-1 r on the tiled factor, then w'w and v'w.
-__global__ void __launch_bounds__(512) mse_point_kernel(const double* __restrict__ Xt,
-                                                        const double* __restrict__ X, int n, int d,
-                                                        const double* __restrict__ theta, double p,
-                                                        double sigma2,
-                                                        const double* __restrict__ tiles,
-                                                        const double* __restrict__ v, double vtv,
-                                                        double* __restrict__ mse, int* bad) {
-  extern __shared__ double w[];
-  __shared__ double red[2][16];
-  const int j = blockIdx.x;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < d; ++k) {
-      const double term = pow_abs_p(Xt[(size_t)j * d + k] - X[(size_t)i * d + k], p);
-      s = __dadd_rn(s, __dmul_rn(theta[k], term));
-    }
-    const double r = exp_neg(s);
-    if (!isfinite(r)) *bad = 1;
-    w[i] = r;
-  }
-  __syncthreads();
-  auto Lat = [&](int i, int c) {
-    return tiles[tile_index(i >> 7, c >> 7) * TILE_ELEMS + elem_off(i & 127, c & 127)];
-  };
-  for (int k = 0; k < n; ++k) {
-    const double xk = w[k] / Lat(k, k);
-    __syncthreads();
-    for (int l = k + 1 + threadIdx.x; l < n; l += blockDim.x) w[l] -= Lat(l, k) * xk;
-    if (threadIdx.x == 0) w[k] = xk;
-    __syncthreads();
-  }
-  double wtw = 0.0, vtw = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    wtw = fma(w[i], w[i], wtw);
-    vtw = fma(v[i], w[i], vtw);
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int off = 16; off > 0; off >>= 1) {
-    wtw += __shfl_down_sync(0xffffffffu, wtw, off);
-    vtw += __shfl_down_sync(0xffffffffu, vtw, off);
-  }
-  if (lane == 0) {
-    red[0][warp] = wtw;
-    red[1][warp] = vtw;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) {
-      a += red[0][q];
-      b += red[1][q];
-    }
-    const double one_minus = 1.0 - b;
-    double s2 = sigma2 * (1.0 - a + one_minus * one_minus / vtv);
-    mse[j] = s2 < 0.0 ? 0.0 : s2;
-  }
-}
-
-void launch_predict_mse(const double* Xt, int N, const double* X, int n, int d,
-                        const double* theta, double p, double sigma2, const double* tiles, int NT,
-                        const double* v, double vtv, double* work, double* mse, int* bad,
-                        cudaStream_t s) {
-  (void)NT;
-  (void)work;
-  if (N <= 0) return;
-  const size_t smem = (size_t)n * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(mse_point_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  mse_point_kernel<<<N, 512, smem, s>>>(Xt, X, n, d, theta, p, sigma2, tiles, v, vtv, mse, bad);
-}
-
 }  // namespace gpemu_dev
 
 namespace gpemu_dev {
