@@ -293,6 +293,40 @@ __device__ __forceinline__ void window_afrags(const double (&acc)[2][16][2], dou
   }
 }
 
+// The same three helpers for a window at absolute n-tile w (fully unrolled callers: no
+// register rotation needed).
+__device__ __forceinline__ void stage_out_at(const double (&acc)[2][16][2], int w, double* St, int lr, int lc) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nsub = 0; nsub < 2; ++nsub)
+      *reinterpret_cast<double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc) =
+          make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1]);
+}
+__device__ __forceinline__ void stage_in_at(double (&acc)[2][16][2], int w, const double* St, int lr, int lc) {
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int nsub = 0; nsub < 2; ++nsub) {
+      const double2 v = *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc);
+      acc[mi][w + nsub][0] = v.x;
+      acc[mi][w + nsub][1] = v.y;
+    }
+}
+__device__ __forceinline__ void window_afrags_at(const double (&acc)[2][16][2], int w, double (&av)[2][4], int lane) {
+  const int lc = lane & 3, qbase = lane & ~3;
+#pragma unroll
+  for (int ks = 0; ks < 4; ++ks) {
+    const int src = qbase | (2 * (ks & 1) + (lc >> 1));
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const double v0 = __shfl_sync(0xffffffffu, acc[mi][w + (ks >> 1)][0], src);
+      const double v1 = __shfl_sync(0xffffffffu, acc[mi][w + (ks >> 1)][1], src);
+      av[mi][ks] = -((lc & 1) ? v1 : v0);
+    }
+  }
+}
+
 __device__ __forceinline__ void rotate_window(double (&acc)[2][16][2]) {
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
@@ -738,11 +772,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             Dd[q] = cc <= rr ? Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)] : 0.0;
           }
           consumer_sync();
+          // Fully unrolled over the eight 16-column blocks: window n-tiles w = 2cb, 2cb+1 are
+          // compile-time register indices (no rotation), and every L(j,j) operand address is a
+          // per-lane base plus an immediate, so the DMMAs of independent column blocks
+          // interleave instead of queueing behind runtime predicates.
+          const int lane_base = (lr << 5) + lc;
+#pragma unroll
           for (int cb = 0; cb < 8; ++cb) {
-            const int o = 16 * cb;
-            // (a) columns o..o+15 (acc[mi][0..1], rotated window): through the warp's
-            // staging block so lane r < 16 owns row r and substitutes in registers
-            stage_out(acc, St, lr, lc);
+            const int o = 16 * cb, w = 2 * cb;
+            // (a) columns o..o+15 (acc[mi][w..w+1]): through the warp's staging block so
+            // lane r < 16 owns row r and substitutes in registers
+            stage_out_at(acc, w, St, lr, lc);
             __syncwarp();
             if (lane < 16) {
               double xr[16];
@@ -751,21 +791,21 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               store_row16(xr, St + lane * kStageLd);
             }
             __syncwarp();
-            stage_in(acc, St, lr, lc);
-            // (b) acc[:, 2..] -= X_block * L(j,j)[rows right of the block, block cols]^T
+            stage_in_at(acc, w, St, lr, lc);
+            // (b) acc[:, a] -= X_block * L(j,j)[8a + lr, block cols]^T for the n-tiles a right
+            // of the block (element (8a + lr, o + 4ks + lc) of the swizzled tile layout)
             if (cb < 7) {
               double av[2][4];
-              window_afrags(acc, av, lane);
+              window_afrags_at(acc, w, av, lane);
 #pragma unroll
-              for (int nb = 2; nb < 16; ++nb) {
-                if (nb < 16 - 2 * cb) {
-                  const int nrow = o + 8 * nb + lr;  // row of L(j,j) = output column
+              for (int ks = 0; ks < 4; ++ks) {
+                const double* Lk = Ls + ((cb >> 1) << 12) + lane_base +
+                                   (((((o >> 2) + ks) & 7) ^ lr) << 2);
 #pragma unroll
-                  for (int ks = 0; ks < 4; ++ks) {
-                    const double b = Ls[elem_off(nrow, o + 4 * ks + lc)];
-                    dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
-                    dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
-                  }
+                for (int a = w + 2; a < 16; ++a) {
+                  const double b = Lk[a << 8];
+                  dmma884(acc[0][a][0], acc[0][a][1], av[0][ks], b);
+                  dmma884(acc[1][a][0], acc[1][a][1], av[1][ks], b);
                 }
               }
             }
@@ -774,10 +814,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
               for (int nsub = 0; nsub < 2; ++nsub)
-                __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, 2 * cb + nsub, lc)),
-                       make_double2(acc[mi][nsub][0], acc[mi][nsub][1]));
-            // (d) rotate the window by one 16-column block
-            rotate_window(acc);
+                __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, w + nsub, lc)),
+                       make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1]));
           }
           if (tid == 0) pr.lap(PR_TRSM);
         }
