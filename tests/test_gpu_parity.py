@@ -357,3 +357,30 @@ def test_eval_batch_extra_shapes(g, name, engine):
     fin = np.isfinite(z["neg2"])
     assert rel(r["mu"][fin], z["mu"][fin]) < 1e-6
     ev.close()
+
+
+def test_c4_full_size_vs_reference(g, ctx):
+    """Largest config at full size (C4: n=16384, d=20, p=1.9, nugget 1e-8): the deviance record
+    of two thetas against the reference's own evaluation (tests/golden/c4_full.npz,
+    tools/make_golden_c4.py), gated on the reference's self-discrepancy between its two builds;
+    plus batch invariance at this size."""
+    path = os.path.join(GOLD, "c4_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("c4_full golden not generated")
+    z = np.load(path)
+    n, d = int(z["n"]), int(z["d"])
+    rng = np.random.default_rng(int(z["seed"]))
+    X = np.empty((n, d))
+    for k in range(d):
+        X[:, k] = (rng.permutation(n) + rng.random(n)) / n
+    y = (np.sin(3.0 * X + 0.37 * np.arange(d)) + 0.5 * X * X).sum(1)
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), float(z["p"]), float(z["nugget"]), g.Backend(ctx),
+                            max_batch=2)
+    r = ev.eval_batch(z["thetas"])
+    assert np.array_equal(r["jitter"], z["jitter_strict"])
+    for k, floor in (("neg2", 1e-9), ("log_det", 1e-9), ("mu", 1e-8), ("sigma2", 1e-8)):
+        self_disc = rel(z[f"{k}_strict"], z[f"{k}_fast"])
+        assert rel(r[k], z[f"{k}_strict"]) <= max(floor, 10 * self_disc), k
+    r1 = ev.eval_batch(z["thetas"][1:])
+    assert r1["neg2"][0] == r["neg2"][1]  # slot 0 of a batch of 1 == slot 1 of a batch of 2
+    ev.close()
