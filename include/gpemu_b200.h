@@ -98,6 +98,17 @@ GPEMU_API int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const
  * |dx|^p table on the device. max_batch bounds the candidates per eval call. */
 GPEMU_API int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
                       double p, double nugget, size_t max_batch, gpemu_plan** out);
+
+/* Working precision of a plan (core.hpp:86-96 Precision; FitConfig::precision). SINGLE runs
+ * the reference's float instantiation: float design / table / R / factor / solves, log|R|
+ * and the dots in double (likelihood.hpp:74-158, backend.hpp:111-113, matrix.hpp:64-69). */
+typedef enum { GPEMU_PRECISION_DOUBLE = 0, GPEMU_PRECISION_SINGLE = 1 } gpemu_precision;
+
+/* gpemu_plan_create with an explicit working precision. */
+GPEMU_API int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_t n,
+                                   size_t d, double p, double nugget, size_t max_batch,
+                                   int precision, gpemu_plan** out);
+GPEMU_API int gpemu_plan_precision(const gpemu_plan* plan);
 GPEMU_API int gpemu_plan_destroy(gpemu_plan* plan);
 GPEMU_API size_t gpemu_plan_device_bytes(const gpemu_plan* plan);
 

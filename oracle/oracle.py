@@ -311,6 +311,12 @@ class RefLib:
                                      C.c_int, _u64, C.c_int, C.c_uint, _dp, _dp, _dp]
         L.ref_model_predict.argtypes = [_dp, _dp, _sz, _sz, _dp, C.c_double, C.c_double, cs,
                                         C.c_uint, _dp, _sz, _dp, _dp, _dp]
+        # single precision (the reference's float instantiation)
+        L.ref_eval_batch_f32.argtypes = L.ref_eval_batch.argtypes
+        L.ref_eval_batch_timed_f32.argtypes = L.ref_eval_batch_timed.argtypes
+        L.ref_fit_f32.argtypes = [_dp, _dp, _sz, _sz, C.c_double, C.c_double, _dp, _dp, C.c_int,
+                                  C.c_int, _u64, cs, C.c_uint, _dp, _dp, _dp, _dp]
+        L.ref_model_predict_f32.argtypes = L.ref_model_predict.argtypes
 
     def _check(self, rc):
         if rc != 0:
@@ -372,25 +378,29 @@ class RefLib:
         self._check(self.lib.ref_solve(_ptr(L), L.shape[0], _ptr(b), int(upper), _ptr(x)))
         return x
 
-    def eval_batch(self, X, y, thetas, p, nugget=0.0, backend="parallel", threads=1):
+    def eval_batch(self, X, y, thetas, p, nugget=0.0, backend="parallel", threads=1,
+                   precision="double"):
         X, y, thetas = _f64(X), _f64(y), _f64(np.atleast_2d(thetas))
         n, d = X.shape
         B = thetas.shape[0]
         out = {k: np.empty(B) for k in ("neg2", "mu", "sigma2", "jitter", "log_det")}
-        self._check(self.lib.ref_eval_batch(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
+        fn = self.lib.ref_eval_batch_f32 if precision == "single" else self.lib.ref_eval_batch
+        self._check(fn(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
                                             backend.encode(), threads, _ptr(out["neg2"]),
                                             _ptr(out["mu"]), _ptr(out["sigma2"]),
                                             _ptr(out["jitter"]), _ptr(out["log_det"])))
         return out
 
-    def eval_batch_timed(self, X, y, thetas, p, nugget=0.0, backend="parallel", threads=0):
+    def eval_batch_timed(self, X, y, thetas, p, nugget=0.0, backend="parallel", threads=0,
+                         precision="double"):
         """-> (neg2, seconds_plan, seconds_evals); threads=0 = hardware_concurrency."""
         X, y, thetas = _f64(X), _f64(y), _f64(np.atleast_2d(thetas))
         n, d = X.shape
         B = thetas.shape[0]
         neg2 = np.empty(B)
         sp, se = C.c_double(), C.c_double()
-        self._check(self.lib.ref_eval_batch_timed(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
+        fn = self.lib.ref_eval_batch_timed_f32 if precision == "single" else self.lib.ref_eval_batch_timed
+        self._check(fn(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(thetas), B,
                                                   backend.encode(), threads, _ptr(neg2),
                                                   C.byref(sp), C.byref(se)))
         return neg2, sp.value, se.value
@@ -425,7 +435,22 @@ class RefLib:
                                             _ptr(tr), _ptr(sc)))
         return tf, sc[0], tr, sc[1], int(sc[2])
 
-    def model_predict(self, X, y, theta, p, nugget, Xtest, backend="parallel", threads=1):
+    def fit_f32(self, X, y, p=1.95, nugget=0.0, lo=1e-6, hi=12.0, population=100, generations=20,
+                seed=0, backend="parallel", threads=1):
+        """fit_gp_detailed<float> (FitConfig::precision = single)."""
+        X, y = _f64(X), _f64(y)
+        n, d = X.shape
+        lo = _f64(np.broadcast_to(lo, (d,)))
+        hi = _f64(np.broadcast_to(hi, (d,)))
+        theta, sc, alpha, tb = np.empty(d), np.empty(4), np.empty(n), np.empty(generations)
+        self._check(self.lib.ref_fit_f32(_ptr(X), _ptr(y), n, d, p, nugget, _ptr(lo), _ptr(hi),
+                                         population, generations, seed, backend.encode(), threads,
+                                         _ptr(theta), _ptr(sc), _ptr(alpha), _ptr(tb)))
+        return dict(theta=theta, neg2=sc[0], mu=sc[1], sigma2=sc[2], jitter_max=sc[3], alpha=alpha,
+                    trace_best=tb)
+
+    def model_predict(self, X, y, theta, p, nugget, Xtest, backend="parallel", threads=1,
+                      precision="double"):
         X, y, theta = _f64(X), _f64(y), _f64(theta)
         n, d = X.shape
         Xtest = _f64(Xtest) if Xtest is not None else np.empty((0, d))
@@ -433,7 +458,8 @@ class RefLib:
         yhat = np.empty(N)
         sc = np.empty(4)
         alpha = np.empty(n)
-        self._check(self.lib.ref_model_predict(_ptr(X), _ptr(y), n, d, _ptr(theta), p, nugget,
+        fn = self.lib.ref_model_predict_f32 if precision == "single" else self.lib.ref_model_predict
+        self._check(fn(_ptr(X), _ptr(y), n, d, _ptr(theta), p, nugget,
                                                backend.encode(), threads, _ptr(Xtest), N,
                                                _ptr(yhat), _ptr(sc), _ptr(alpha)))
         return dict(yhat=yhat, neg2=sc[0], mu=sc[1], sigma2=sc[2], jitter=sc[3], alpha=alpha)

@@ -275,4 +275,98 @@ REF_API int ref_model_predict(const double* X, const double* y, std::size_t n, s
   REF_CATCH
 }
 
+// ---- single precision (Precision::kSingle, the reference's float instantiation) ----------
+// ProfileEvaluator<float> / fit_gp_detailed<float> / model_at_theta<float> + predict, as the
+// bench runs them for precision = single (bench.hpp:489-490).
+REF_API int ref_eval_batch_f32(const double* X, const double* y, std::size_t n, std::size_t d, double p,
+                               double nugget, const double* thetas, std::size_t B, const char* backend,
+                               unsigned threads, double* neg2, double* mu, double* sigma2, double* jitter,
+                               double* log_det) {
+  REF_TRY
+  auto be = make_backend<float>(backend, threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  ProfileEvaluator<float> ev(data, p, nugget, *be);
+  for (std::size_t b = 0; b < B; ++b) {
+    const auto r = ev.eval(std::span<const double>(thetas + b * d, d));
+    neg2[b] = r.neg2_log_lik;
+    if (mu) mu[b] = r.mu_hat;
+    if (sigma2) sigma2[b] = r.sigma2_hat;
+    if (jitter) jitter[b] = r.jitter_used;
+    if (log_det) log_det[b] = std::isfinite(r.neg2_log_lik) ? ev.last_factor().log_det : 0.0;
+  }
+  return 0;
+  REF_CATCH
+}
+
+REF_API int ref_eval_batch_timed_f32(const double* X, const double* y, std::size_t n, std::size_t d,
+                                     double p, double nugget, const double* thetas, std::size_t B,
+                                     const char* backend, unsigned threads, double* neg2,
+                                     double* seconds_plan, double* seconds_evals) {
+  REF_TRY
+  auto be = make_backend<float>(backend, threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  const auto t0 = std::chrono::steady_clock::now();
+  ProfileEvaluator<float> ev(data, p, nugget, *be);
+  const auto t1 = std::chrono::steady_clock::now();
+  for (std::size_t b = 0; b < B; ++b) neg2[b] = ev.eval(std::span<const double>(thetas + b * d, d)).neg2_log_lik;
+  const auto t2 = std::chrono::steady_clock::now();
+  *seconds_plan = std::chrono::duration<double>(t1 - t0).count();
+  *seconds_evals = std::chrono::duration<double>(t2 - t1).count();
+  return 0;
+  REF_CATCH
+}
+
+REF_API int ref_fit_f32(const double* X, const double* y, std::size_t n, std::size_t d, double p, double nugget,
+                        const double* lo, const double* hi, int population, int generations, std::uint64_t seed,
+                        const char* backend, unsigned threads, double* theta_hat,
+                        double* scalars /*neg2,mu,sigma2,jitter_max*/, double* alpha, double* trace_best) {
+  REF_TRY
+  auto be = make_backend<float>(backend, threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  FitConfig cfg;
+  cfg.precision = Precision::kSingle;
+  cfg.ga.population = population;
+  cfg.ga.generations = generations;
+  cfg.seed = seed;
+  cfg.p = p;
+  cfg.nugget = nugget;
+  cfg.theta_bounds.resize(d);
+  for (std::size_t k = 0; k < d; ++k) cfg.theta_bounds[k] = {lo[k], hi[k]};
+  const auto fit = fit_gp_detailed(data, cfg, *be);
+  for (std::size_t k = 0; k < d; ++k) theta_hat[k] = fit.model.params.theta[k];
+  scalars[0] = fit.model.neg2_log_lik;
+  scalars[1] = fit.model.mu_hat;
+  scalars[2] = fit.model.sigma2_hat;
+  scalars[3] = fit.jitter_max;
+  for (std::size_t i = 0; i < n; ++i) alpha[i] = static_cast<double>(fit.model.alpha[i]);
+  for (std::size_t g = 0; g < fit.trace.generations.size(); ++g)
+    if (trace_best) trace_best[g] = fit.trace.generations[g].best_value;
+  return 0;
+  REF_CATCH
+}
+
+REF_API int ref_model_predict_f32(const double* X, const double* y, std::size_t n, std::size_t d,
+                                  const double* theta, double p, double nugget, const char* backend,
+                                  unsigned threads, const double* Xtest, std::size_t N, double* yhat,
+                                  double* scalars /*neg2,mu,sigma2,jitter*/, double* alpha) {
+  REF_TRY
+  auto be = make_backend<float>(backend, threads);
+  const Dataset data = new_dataset(to_matrix(X, n, d), std::vector<double>(y, y + n));
+  const auto model = model_at_theta(data, std::span<const double>(theta, d), p, nugget, *be);
+  if (scalars) {
+    scalars[0] = model.neg2_log_lik;
+    scalars[1] = model.mu_hat;
+    scalars[2] = model.sigma2_hat;
+    scalars[3] = model.factor.jitter_used;
+  }
+  if (alpha)
+    for (std::size_t i = 0; i < n; ++i) alpha[i] = static_cast<double>(model.alpha[i]);
+  if (N) {
+    const auto pr = predict(model, to_matrix(Xtest, N, d), be->pool());
+    std::memcpy(yhat, pr.data(), N * sizeof(double));
+  }
+  return 0;
+  REF_CATCH
+}
+
 }  // extern "C"

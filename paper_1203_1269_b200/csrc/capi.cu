@@ -146,6 +146,8 @@ struct gpemu_plan {
   int epoch = 0;
   DevBuf<double> X, y, table, factors, borders, theta, jitter, out;
   DevBuf<int> status, slots, flags, counter, error;
+  int precision = GPEMU_PRECISION_DOUBLE;
+  DevBuf<float> factors_f, borders_f;  // single precision storage (table: `table`, double)
   DevBuf<unsigned long long> dag_prof;  // optional DAG phase counters
   std::vector<double> h_jitter;
   std::vector<int> h_slots, h_status_all;
@@ -192,6 +194,7 @@ struct gpemu_model {
   DevBuf<double> ext;
   DevBuf<int> ext_flags, ext_slot, counter, error;
   int ext_rt_cap = 0, epoch = 0;
+  bool single = false;  // float model: yhat through the float corr_vector / dot (predict_f32)
   // predict scratch, grown on demand and reused across calls (no per-call cudaMalloc/Free)
   DevBuf<double> pred_xt, pred_y, pred_mse, pred_part;
   DevBuf<int> pred_bad;
@@ -220,7 +223,13 @@ void run_chol(gpemu_plan* pl, int nact) {
     a.trace = a.prof + (size_t)pl->ctx->num_sms * 24 + 256;
     a.trace_cap = kTraceTasks;
   }
-  if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
+  if (pl->precision == GPEMU_PRECISION_SINGLE) {
+    a.factors = reinterpret_cast<double*>(pl->factors_f.p);
+    a.borders = reinterpret_cast<double*>(pl->borders_f.p);
+    a.prof = nullptr;
+    a.trace = nullptr;
+    launch_chol_dag_f32(a, pl->ctx->num_sms, pl->ctx->stream);
+  } else if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
     launch_chol_simple(a, pl->ctx->stream);
   } else {
     launch_chol_dag(a, pl->ctx->num_sms, pl->ctx->stream);
@@ -252,16 +261,25 @@ int run_batch(gpemu_plan* pl, size_t B) {
     ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), nact * sizeof(int), cudaMemcpyHostToDevice, s),
        "H2D slots");
     pl->mark_begin(0);
-    launch_assemble(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
-                    pl->slots.p, nact, pl->jitter.p, pl->factors.p, pl->slot_stride,
-                    pl->borders.p, pl->status.p, s);
+    if (pl->precision == GPEMU_PRECISION_SINGLE)
+      launch_assemble_f32(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
+                          pl->slots.p, nact, pl->jitter.p, pl->factors_f.p, pl->slot_stride,
+                          pl->borders_f.p, pl->status.p, s);
+    else
+      launch_assemble(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
+                      pl->slots.p, nact, pl->jitter.p, pl->factors.p, pl->slot_stride,
+                      pl->borders.p, pl->status.p, s);
     pl->mark_end();
     pl->mark_begin(1);
     run_chol(pl, nact);
     pl->mark_end();
     pl->mark_begin(2);
-    launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
-                    pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+    if (pl->precision == GPEMU_PRECISION_SINGLE)
+      launch_finalize_f32(pl->factors_f.p, pl->slot_stride, pl->borders_f.p, pl->status.p,
+                          pl->jitter.p, pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+    else
+      launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
+                      pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
     pl->mark_end();
     pl->ctx->launches += 4;
     ck(cudaGetLastError(), "kernel launch");
@@ -339,6 +357,25 @@ gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const dou
   m->v.alloc(pl->Npad);
   ck(cudaMemcpyAsync(m->X.p, pl->X.p, (size_t)pl->n * pl->d * sizeof(double), cudaMemcpyDeviceToDevice, s), "model X");
   ck(cudaMemcpyAsync(m->theta_d.p, theta, pl->d * sizeof(double), cudaMemcpyHostToDevice, s), "model theta");
+  if (pl->precision == GPEMU_PRECISION_SINGLE) {
+    // float factor: alpha by the float solves (likelihood.hpp:228-229); the factor and the
+    // border rows widened to double for the MSE extension DAG
+    m->single = true;
+    const float* ftiles = pl->factors_f.p + (size_t)slot * pl->slot_stride;
+    launch_tiles_f32_to_f64(ftiles, pl->NT, m->tiles.p, s);
+    std::vector<float> hb(2 * (size_t)pl->Npad);
+    ck(cudaMemcpyAsync(hb.data(), pl->borders_f.p + (size_t)slot * 2 * pl->Npad, hb.size() * sizeof(float),
+                       cudaMemcpyDeviceToHost, s), "D2H borders");
+    ck(cudaStreamSynchronize(s), "borders");
+    std::vector<double> hu(hb.begin(), hb.begin() + pl->Npad), hv(hb.begin() + pl->Npad, hb.end());
+    ck(cudaMemcpy(m->u.p, hu.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice), "model u");
+    ck(cudaMemcpy(m->v.p, hv.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice), "model v");
+    launch_alpha_f32(ftiles, pl->n, pl->y.p, m->mu, m->alpha.p, s);
+    pl->ctx->launches += 2;
+    ck(cudaStreamSynchronize(s), "float model");
+    pl->solves += 2;
+    return m;
+  }
   ck(cudaMemcpyAsync(m->tiles.p, pl->factors.p + (size_t)slot * pl->slot_stride,
                      pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
      "model tiles");
@@ -608,7 +645,16 @@ int gpemu_solve_upper(gpemu_ctx* ctx, const double* L, size_t n, const double* b
 // ---------------------------------------------------------------------------
 int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
                       double p, double nugget, size_t max_batch, gpemu_plan** out) {
+  return gpemu_plan_create_ex(ctx, X, y, n, d, p, nugget, max_batch, GPEMU_PRECISION_DOUBLE, out);
+}
+
+int gpemu_plan_precision(const gpemu_plan* pl) { return pl ? pl->precision : -1; }
+
+int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_t n, size_t d,
+                         double p, double nugget, size_t max_batch, int precision, gpemu_plan** out) {
   GPEMU_GUARD_BEGIN
+  if (precision != GPEMU_PRECISION_DOUBLE && precision != GPEMU_PRECISION_SINGLE)
+    return set_error(GPEMU_CONFIG, "unknown precision %d (expected single|double)", precision);
   if (!ctx || !X || !y || !out) return set_error(GPEMU_VALIDATION, "plan_create: null argument");
   if (n < 2) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 2 design points");
   if (d < 1) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 1 input dimension");
@@ -636,9 +682,16 @@ int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n
   try {
     pl->X.alloc(n * d);
     pl->y.alloc(n);
-    pl->table.alloc((size_t)num_tiles(pl->NT) * d * TILE_ELEMS);
-    pl->factors.alloc(pl->nslots * pl->slot_stride);
-    pl->borders.alloc(pl->nslots * 2 * pl->Npad);
+    pl->precision = precision;
+    if (precision == GPEMU_PRECISION_SINGLE) {
+      pl->table.alloc((size_t)num_tiles(pl->NT) * d * TILE_ELEMS);  // column-major, double
+      pl->factors_f.alloc(pl->nslots * pl->slot_stride);
+      pl->borders_f.alloc(pl->nslots * 2 * pl->Npad);
+    } else {
+      pl->table.alloc((size_t)num_tiles(pl->NT) * d * TILE_ELEMS);
+      pl->factors.alloc(pl->nslots * pl->slot_stride);
+      pl->borders.alloc(pl->nslots * 2 * pl->Npad);
+    }
     pl->theta.alloc(pl->nslots * d);
     pl->jitter.alloc(pl->nslots);
     pl->out.alloc(pl->nslots * REC_SIZE);
@@ -657,7 +710,10 @@ int gpemu_plan_create(gpemu_ctx* ctx, const double* X, const double* y, size_t n
   ck(cudaMemsetAsync(pl->flags.p, 0, pl->flags.count * sizeof(int), s), "memset flags");
   ck(cudaMemsetAsync(pl->error.p, 0, sizeof(int), s), "memset error");
   ck(cudaMemsetAsync(pl->status.p, 0, pl->nslots * sizeof(int), s), "memset status");
-  launch_pow_table(pl->X.p, pl->n, pl->d, p, pl->NT, pl->table.p, s);
+  if (precision == GPEMU_PRECISION_SINGLE)
+    launch_pow_table_f32(pl->X.p, pl->n, pl->d, p, pl->NT, pl->table.p, s);
+  else
+    launch_pow_table(pl->X.p, pl->n, pl->d, p, pl->NT, pl->table.p, s);
   ctx->launches += 1;
   ck(cudaGetLastError(), "pow_table launch");
   ck(cudaStreamSynchronize(s), "plan_create");
@@ -680,6 +736,7 @@ size_t gpemu_plan_device_bytes(const gpemu_plan* pl) {
   return (pl->X.count + pl->y.count + pl->table.count + pl->factors.count + pl->borders.count +
           pl->theta.count + pl->jitter.count + pl->out.count) *
              sizeof(double) +
+         (pl->factors_f.count + pl->borders_f.count) * sizeof(float) +
          (pl->status.count + pl->slots.count + pl->flags.count + 2) * sizeof(int);
 }
 
@@ -782,7 +839,10 @@ int gpemu_plan_last_factor(gpemu_plan* pl, size_t slot, double* L_out, double* l
   if (L_out) {
     DevBuf<double> dL;
     dL.alloc((size_t)pl->n * pl->n);
-    launch_tiles_to_rowmajor(pl->factors.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
+    if (pl->precision == GPEMU_PRECISION_SINGLE)
+      launch_tiles_f32_to_rowmajor(pl->factors_f.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
+    else
+      launch_tiles_to_rowmajor(pl->factors.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
     pl->ctx->launches += 1;
     ck(cudaMemcpyAsync(L_out, dL.p, (size_t)pl->n * pl->n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
   }
@@ -1004,14 +1064,25 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
       const double* r = &pl->h_out[(size_t)i * REC_SIZE];
       std::copy(r, r + REC_SIZE, stash_rec.begin());
       std::copy(&thetas[(size_t)i * d], &thetas[(size_t)i * d] + d, stash_theta.begin());
-      ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
-                         pl->factors.p + (size_t)i * pl->slot_stride,
-                         pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
-         "stash factor");
-      ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
-                         pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
-                         cudaMemcpyDeviceToDevice, s),
-         "stash border");
+      if (pl->precision == GPEMU_PRECISION_SINGLE) {
+        ck(cudaMemcpyAsync(pl->factors_f.p + (size_t)stash * pl->slot_stride,
+                           pl->factors_f.p + (size_t)i * pl->slot_stride,
+                           pl->slot_stride * sizeof(float), cudaMemcpyDeviceToDevice, s),
+           "stash factor");
+        ck(cudaMemcpyAsync(pl->borders_f.p + (size_t)stash * 2 * pl->Npad,
+                           pl->borders_f.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(float),
+                           cudaMemcpyDeviceToDevice, s),
+           "stash border");
+      } else {
+        ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
+                           pl->factors.p + (size_t)i * pl->slot_stride,
+                           pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
+           "stash factor");
+        ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
+                           pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
+                           cudaMemcpyDeviceToDevice, s),
+           "stash border");
+      }
     }
   }
   ck(cudaStreamSynchronize(s), "fit");
@@ -1187,10 +1258,17 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   bad.reserve(1);
   ck(cudaMemcpyAsync(dXt.p, Xtest, N * m->d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D Xtest");
   ck(cudaMemsetAsync(bad.p, 0, sizeof(int), s), "memset");
+  if (m->single) {  // float model: corr_vector<float> + dot_accumulate (predictor.hpp:36-44)
+    launch_predict_f32(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
+                       dy.p, bad.p, s);
+    m->ctx->launches += 1;
+  }
   if (!mse) {
-    launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
-                   dpart.p, dy.p, bad.p, s);
-    m->ctx->launches += 2;
+    if (!m->single) {
+      launch_predict(dXt.p, (int)N, m->X.p, m->n, m->d, m->theta_d.p, m->p, m->mu, m->alpha.p,
+                     dpart.p, dy.p, bad.p, s);
+      m->ctx->launches += 2;
+    }
   } else {
     // Cross-correlation tiles r for chunks of test points; yhat = mu + r.alpha from the tiles
     // (predict_kernel's summation order: the same bits as the yhat-only call); then
@@ -1216,7 +1294,7 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
       const int RT = (Nc + TILE - 1) / TILE;
       launch_cross_tiles(dXt.p + p0 * m->d, Nc, m->X.p, m->n, m->d, m->theta_d.p, m->p, NT, RT,
                          m->ext.p, bad.p, s);
-      launch_yhat_tiles(m->ext.p, Nc, m->n, NT, m->alpha.p, dpart.p, N, p0, s);
+      if (!m->single) launch_yhat_tiles(m->ext.p, Nc, m->n, NT, m->alpha.p, dpart.p, N, p0, s);
       DagLaunch a;
       a.factors = m->tiles.p;
       a.borders = nullptr;
@@ -1238,8 +1316,10 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
                         nullptr, dm.p + p0, s);
       m->ctx->launches += 4;
     }
-    launch_predict_combine(dpart.p, (int)N, m->n, m->mu, dy.p, s);
-    m->ctx->launches += 1;
+    if (!m->single) {
+      launch_predict_combine(dpart.p, (int)N, m->n, m->mu, dy.p, s);
+      m->ctx->launches += 1;
+    }
   }
   ck(cudaGetLastError(), "predict launch");
   int hbad = 0;

@@ -95,4 +95,24 @@ void launch_ext_reduce(const double* ext, int N, int n, int NT, const double* u,
                        double mu, double sigma2, double vtv, double* yhat, double* mse,
                        cudaStream_t s);
 
+// ---- single precision (kernels_f32.cu, kernels_chol_f32.cu) ------------------
+// Float tiles are column-major 128 x 128 (element (r, c) at c * 128 + r); same packed-lower
+// tile_index, slots, borders [y; 1] and record layout as the FP64 path.
+// the single-precision plan keeps its |dx|^p table in double (column-major tiles)
+void launch_pow_table_f32(const double* X, int n, int d, double p, int NT, double* table, cudaStream_t s);
+void launch_assemble_f32(const double* table, const double* theta, const double* y, int n, int d,
+                         double nugget, int NT, const int* slots, int nslots, const double* jitter,
+                         float* factors, size_t slot_stride, float* borders, int* status, cudaStream_t s);
+// DagLaunch with factors / borders pointing at float storage; no extension mode.
+void launch_chol_dag_f32(const DagLaunch& a, int num_sms, cudaStream_t s);
+size_t chol_dag_f32_smem_bytes();
+void launch_finalize_f32(const float* factors, size_t slot_stride, const float* borders,
+                         const int* status, const double* jitter, int n, int NT, const int* slots,
+                         int nslots, double* out, cudaStream_t s);
+void launch_alpha_f32(const float* tiles, int n, const double* y, double mu, double* alpha, cudaStream_t s);
+void launch_tiles_f32_to_f64(const float* src, int NT, double* dst, cudaStream_t s);
+void launch_tiles_f32_to_rowmajor(const float* tiles, int n, int NT, double* L, cudaStream_t s);
+void launch_predict_f32(const double* Xt, int N, const double* X, int n, int d, const double* theta,
+                        double p, double mu, const double* alpha, double* yhat, int* bad, cudaStream_t s);
+
 }  // namespace gpemu_dev

@@ -75,6 +75,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
+    "gpemu_plan_create_ex", "gpemu_plan_precision",
 )
 
 
@@ -123,6 +124,9 @@ def lib():
     L.gpemu_solve_upper.argtypes = [_vp, _dp, _sz, _dp, _dp]
     L.gpemu_plan_create.argtypes = [_vp, _dp, _dp, _sz, _sz, C.c_double, C.c_double, _sz,
                                     C.POINTER(_vp)]
+    L.gpemu_plan_create_ex.argtypes = [_vp, _dp, _dp, _sz, _sz, C.c_double, C.c_double, _sz,
+                                       C.c_int, C.POINTER(_vp)]
+    L.gpemu_plan_precision.argtypes = [_vp]
     L.gpemu_plan_destroy.argtypes = [_vp]
     L.gpemu_plan_device_bytes.argtypes = [_vp]
     L.gpemu_plan_device_bytes.restype = _sz
@@ -280,10 +284,24 @@ class GaConfig:
         return self.population * self.generations
 
 
+PRECISIONS = {"double": 0, "single": 1, "float": 1}
+
+
+def parse_precision(s: str) -> str:
+    """core.hpp:92-96: 'single' | 'float' | 'double', else ConfigError."""
+    if s in ("single", "float"):
+        return "single"
+    if s == "double":
+        return "double"
+    raise ConfigError(f"unknown precision '{s}' (expected single|double)")
+
+
 @dataclass
 class FitConfig:
-    """core.hpp:100-124 (precision fixed to double: the north_star path is FP64)."""
+    """core.hpp:100-124. precision 'single' runs the reference's float instantiation on the
+    device's FP32 engine (float R / factor / solves, log|R| and dots in double)."""
     backend: str = "accelerated"
+    precision: str = "double"
     ga: GaConfig = field(default_factory=GaConfig)
     theta_bounds: List[tuple] = field(default_factory=list)
     seed: int = 0
@@ -480,15 +498,17 @@ class ProfileEvaluator:
     """likelihood.hpp:74-158 bound to a device plan. eval_batch is the B200 hot path."""
 
     def __init__(self, data: Dataset, p: float, nugget: float, backend: Backend,
-                 max_batch: int = 128):
+                 max_batch: int = 128, precision: str = "double"):
         self.backend = backend
         self._n, self._d = data.n(), data.d()
         self._data = data
+        self.precision = parse_precision(precision)
         Hyperparameters([1.0] * self._d, p, nugget).validate(self._d)
         h = _vp()
         X, y = _f64(data.inputs()), _f64(data.outputs())
-        _check(lib().gpemu_plan_create(backend.ctx.handle, _p(X), _p(y), self._n, self._d,
-                                       float(p), float(nugget), int(max_batch), C.byref(h)))
+        _check(lib().gpemu_plan_create_ex(backend.ctx.handle, _p(X), _p(y), self._n, self._d,
+                                          float(p), float(nugget), int(max_batch),
+                                          PRECISIONS[self.precision], C.byref(h)))
         self.handle = h
         self.p, self.nugget, self.max_batch = float(p), float(nugget), int(max_batch)
         self._jitter_max = 0.0
@@ -689,7 +709,7 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
     bounds = cfg.bounds_for(d)
     own = evaluator is None
     ev = evaluator or ProfileEvaluator(data, cfg.p, cfg.nugget, backend,
-                                       max_batch=cfg.ga.population)
+                                       max_batch=cfg.ga.population, precision=cfg.precision)
     try:
         lo = _f64([b[0] for b in bounds])
         hi = _f64([b[1] for b in bounds])
@@ -757,9 +777,10 @@ def fit_gp(data: Dataset, cfg: FitConfig, backend: Backend) -> GpModel:
     return fit_gp_detailed(data, cfg, backend).model
 
 
-def model_at_theta(data: Dataset, theta, p: float, nugget: float, backend: Backend) -> GpModel:
-    """likelihood.hpp:216-237."""
-    ev = ProfileEvaluator(data, p, nugget, backend, max_batch=1)
+def model_at_theta(data: Dataset, theta, p: float, nugget: float, backend: Backend,
+                   precision: str = "double") -> GpModel:
+    """likelihood.hpp:216-237 (precision 'single': the float instantiation)."""
+    ev = ProfileEvaluator(data, p, nugget, backend, max_batch=1, precision=precision)
     try:
         th = _f64(theta)
         sc = np.empty(4)

@@ -384,3 +384,70 @@ def test_c4_full_size_vs_reference(g, ctx):
     r1 = ev.eval_batch(z["thetas"][1:])
     assert r1["neg2"][0] == r["neg2"][1]  # slot 0 of a batch of 1 == slot 1 of a batch of 2
     ev.close()
+
+
+# ---------------------------------------------------------------- single precision
+def _f32_case(seed, n, d):
+    rng = np.random.default_rng(seed)
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1) + 0.3 * X[:, 0]
+    th = 10 ** rng.uniform(-1.0, 0.5, size=(12, d))
+    return X, y, th
+
+
+@pytest.mark.parametrize("n,d", [(200, 2), (700, 3), (1100, 5)])
+def test_single_precision_eval_vs_reference(g, ctx, ref_fast, n, d):
+    """Precision::kSingle (core.hpp:86-96): the device float engine against the reference's
+    float instantiation (ProfileEvaluator<float>). Float results differ from double by the
+    float path's own error, so the gate is relative to it: per candidate with the same jitter
+    step |dev - ref_f32| <= max(1e-5, 10 |ref_f32 - ref_f64|) (relative), and in aggregate
+    the device float is at least as close to the double result as the reference float."""
+    X, y, th = _f32_case(n + d, n, d)
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=12,
+                            precision="single")
+    r = ev.eval_batch(th)
+    fs = ref_fast.eval_batch(X, y, th, 1.95, threads=0, precision="single")
+    fd = ref_fast.eval_batch(X, y, th, 1.95, threads=0)
+    same = r["jitter"] == fs["jitter"]
+    assert same.sum() >= len(th) - 2  # float pivots near the ladder threshold may differ
+    ref_err = np.abs(fs["neg2"] - fd["neg2"]) / np.abs(fd["neg2"])
+    dev_vs_ref = np.abs(r["neg2"] - fs["neg2"]) / np.abs(fs["neg2"])
+    assert np.all(dev_vs_ref[same] <= np.maximum(1e-5, 10 * ref_err[same]))
+    dev_err = np.abs(r["neg2"] - fd["neg2"]) / np.abs(fd["neg2"])
+    assert np.median(dev_err) <= 1.5 * np.median(ref_err) + 1e-7
+    ev.close()
+
+
+def test_single_precision_model_predict(g, ctx, ref_fast):
+    """model_at_theta<float> + predict (predictor.hpp:20-50) against the reference float model."""
+    X, y, th = _f32_case(7, 500, 3)
+    Xt = np.random.default_rng(8).random((300, 3))
+    m = g.model_at_theta(g.new_dataset(X, y), th[0], 1.95, 0.0, g.Backend(ctx), precision="single")
+    rf = ref_fast.model_predict(X, y, th[0], 1.95, 0.0, Xt, threads=0, precision="single")
+    rd = ref_fast.model_predict(X, y, th[0], 1.95, 0.0, Xt, threads=0)
+    yhat, mse = g.predict(m, Xt, with_mse=True)
+    scale = max(np.abs(rd["yhat"]).max(), np.abs(y).max())
+    ref_err = np.max(np.abs(rf["yhat"] - rd["yhat"])) / scale
+    assert np.max(np.abs(yhat - rd["yhat"])) / scale <= max(1e-5, 3 * ref_err)
+    assert np.all(mse >= 0.0)
+    m.close()
+
+
+def test_single_precision_fit(g, ctx, ref_fast):
+    """fit_gp_detailed<float> on the device. A small GA in float is path-dependent (fitness
+    noise ~1e-3 changes selections), so trajectories are not compared; instead the reported
+    float deviance at the device's theta-hat must match the reference float instantiation's
+    evaluation there, within the float gate, and the fit must spend the GA budget."""
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    X, y = z["X"], z["y"]
+    be = g.Backend(ctx)
+    cfg = g.FitConfig(ga=g.GaConfig(population=20, generations=5), seed=3, p=1.95, precision="single")
+    fr = g.fit_gp_detailed(g.new_dataset(X, y), cfg, be)
+    th = np.array([fr.model.params.theta])
+    fs = ref_fast.eval_batch(X, y, th, 1.95, threads=0, precision="single")
+    fd = ref_fast.eval_batch(X, y, th, 1.95, threads=0)
+    ref_err = abs(fs["neg2"][0] - fd["neg2"][0]) / abs(fd["neg2"][0])
+    assert abs(fr.model.neg2_log_lik - fs["neg2"][0]) <= max(1e-5, 10 * ref_err) * abs(fs["neg2"][0])
+    assert fr.ledger.factorizations == 100
+    yhat = g.predict(fr.model, X[:20])  # the float model interpolates its design
+    assert np.max(np.abs(yhat - y[:20])) <= 1e-2 * np.abs(y).max()
