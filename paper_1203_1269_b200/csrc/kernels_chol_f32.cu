@@ -15,7 +15,7 @@
 //     register block rows 16w + 8rg.., cols 8cg..: per k it reads 8 A and 8 B floats (four
 //     LDS.128, A broadcast across the half-warp) for 64 FFMAs;
 //   * <= 128 registers so two CTAs share an SM;
-//   * DIAG: unblocked right-looking POTRF of the tile in shared memory (pivot test !(s > 0),
+//   * DIAG: blocked (16-column) POTRF of the tile in shared memory (pivot test !(s > 0),
 //     backend.hpp:238; IEEE sqrt and division), border rows solved by two warps;
 //   * OFF: X = C L(j,j)^-T in 8-column blocks: the two lanes holding a block substitute their
 //     rows (IEEE division), publish the block through a per-warp buffer, lanes to the right
@@ -108,6 +108,92 @@ __device__ __forceinline__ void ld8(float (&v)[8], const float* p) {
   const float4 b = *reinterpret_cast<const float4*>(p + 4);
   v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
   v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+
+// a / d given r ~ 1/d (IEEE reciprocal): one FMA residual correction gives the rounding of
+// the true quotient (the reference divides, backend.hpp:206 / :138).
+__device__ __forceinline__ float div_by_f(float a, float d, float r) {
+  const float q0 = a * r;
+  return fmaf(fmaf(-q0, d, a), r, q0);
+}
+
+// DIAG POTRF of the column-major tile C in shared memory (lower triangle), blocked in
+// 16-column steps with three CTA barriers per step: (i) warp 0 factors the 16 x 16 diagonal
+// block in registers (lane r holds row r, columns broadcast by shuffles); (ii) one thread per
+// row solves the panel below against it; (iii) the trailing lower triangle is updated with
+// the 16-wide panel, each thread owning 4 rows (strided, conflict-free) of one column at a
+// time (the column's panel values are read once for the 4 rows). Pivot test !(s > 0) as backend.hpp:238. Returns
+// false (uniform) on a failed pivot.
+__device__ __noinline__ bool potrf_tile_f32(float* C, int* fail) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int kb = 0; kb < 8; ++kb) {
+    const int o = 16 * kb;
+    if (warp == 0) {
+      float xr[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) xr[c] = lane < 16 ? C[(o + c) * TILE + o + lane] : 1.0f;
+      bool ok = true;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        float s = __shfl_sync(0xffffffffu, xr[c], c);
+        ok = ok && s > 0.0f;
+        if (!ok) s = 1.0f;
+        const float d = __fsqrt_rn(s);
+        if (lane == c) xr[c] = d;
+        if (lane > c) xr[c] = __fdiv_rn(xr[c], d);
+#pragma unroll
+        for (int c2 = c + 1; c2 < 16; ++c2) {
+          const float l = __shfl_sync(0xffffffffu, xr[c], c2);  // L[c2][c]
+          if (lane >= c2) xr[c2] = fmaf(-xr[c], l, xr[c2]);
+        }
+      }
+      if (lane < 16) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) C[(o + c) * TILE + o + lane] = xr[c];
+      }
+      if (!ok && lane == 0) *fail = 1;
+    }
+    csync();
+    if (*fail) return false;
+    const int r0 = o + 16, m = TILE - r0;  // rows below the diagonal block
+    if (tid < m) {  // (ii) panel: row r, X = A L_bb^-T
+      const int r = r0 + tid;
+      float xr[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) xr[c] = C[(o + c) * TILE + r];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        xr[c] = __fdiv_rn(xr[c], C[(o + c) * TILE + o + c]);
+#pragma unroll
+        for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] = fmaf(-xr[c], C[(o + c) * TILE + o + c2], xr[c2]);
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) C[(o + c) * TILE + r] = xr[c];
+    }
+    csync();
+    if (m > 0) {  // (iii) trailing: C[r][c] -= sum_k L[r][o+k] L[c][o+k], r0 <= c <= r
+      const int groups = (m + 3) / 4;  // a thread owns rows r0 + g + q * groups, q < 4
+      for (int w = tid; w < groups * m; w += kThreadsF) {
+        const int g = w % groups, cc = w / groups;
+        const int c = r0 + cc;
+        if (r0 + g + 3 * groups < c) continue;  // all four rows are above the diagonal
+        float lc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) lc[k] = C[(o + k) * TILE + c];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = r0 + g + q * groups;
+          if (r < c || r >= TILE) continue;
+          float s = C[c * TILE + r];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) s = fmaf(-C[(o + k) * TILE + r], lc[k], s);
+          C[c * TILE + r] = s;
+        }
+      }
+    }
+    csync();
+  }
+  return true;
 }
 
 __global__ void __launch_bounds__(kThreadsF, 2) chol_dag_f32_kernel(DagLaunch a) {
@@ -248,25 +334,7 @@ __global__ void __launch_bounds__(kThreadsF, 2) chol_dag_f32_kernel(DagLaunch a)
       csync();
       bool ok = !skip;
       if (!skip) {
-        // unblocked right-looking POTRF on the column-major tile (lower triangle)
-        const int r = tid & 127, g = tid >> 7;
-        for (int c = 0; c < TILE; ++c) {
-          const float s = C[c * TILE + c];
-          if (!(s > 0.f)) {  // uniform: every thread reads the same pivot
-            ok = false;
-            break;
-          }
-          const float d = __fsqrt_rn(s);
-          if (g == 0 && r > c) C[c * TILE + r] = __fdiv_rn(C[c * TILE + r], d);
-          csync();
-          if (tid == 0) C[c * TILE + c] = d;
-          if (r > c) {
-            const float lr = C[c * TILE + r];
-            for (int c2 = c + 1 + g; c2 <= r; c2 += 2)
-              C[c2 * TILE + r] = fmaf(-lr, C[c * TILE + c2], C[c2 * TILE + r]);
-          }
-          csync();
-        }
+        ok = potrf_tile_f32(C, &misc->fail);
         if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
         csync();
       }
@@ -304,6 +372,9 @@ __global__ void __launch_bounds__(kThreadsF, 2) chol_dag_f32_kernel(DagLaunch a)
         mbar_wait(ljj_bar, misc->ljj_phase & 1);
       }
       const bool run = !skip && *((volatile int*)&a.status[slot]) == 0;
+      float* rinv = W;  // 1 / L_cc (IEEE), read by the substituting lanes
+      if (run && tid < TILE) rinv[tid] = __frcp_rn(C[tid * TILE + tid]);
+      csync();
       if (run) {
         const float* L = C;  // L(j,j), column-major
         for (int cb = 0; cb < 16; ++cb) {
@@ -311,9 +382,9 @@ __global__ void __launch_bounds__(kThreadsF, 2) chol_dag_f32_kernel(DagLaunch a)
           if (cg == cb) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const float dcc = L[(C0 + c) * TILE + C0 + c];
+              const float dcc = L[(C0 + c) * TILE + C0 + c], rcc = rinv[C0 + c];
 #pragma unroll
-              for (int r = 0; r < 8; ++r) acc[r][c] = __fdiv_rn(acc[r][c], dcc);
+              for (int r = 0; r < 8; ++r) acc[r][c] = div_by_f(acc[r][c], dcc, rcc);
 #pragma unroll
               for (int c2 = c + 1; c2 < 8; ++c2) {
                 const float l = L[(C0 + c) * TILE + C0 + c2];
