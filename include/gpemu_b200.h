@@ -188,6 +188,13 @@ GPEMU_API int gpemu_refine_fit(gpemu_plan* plan, const double* lo, const double*
                                const double* theta_fit, double neg2_fit, int budget,
                                double* theta_out, double* neg2_out, int* evals_out,
                                gpemu_model** model_out, double* scalars, double* alpha);
+/* As gpemu_refine_fit, with the polish evaluations on `polish` (the reference polishes in
+ * double regardless of the run precision, bench.hpp:300-301) and the model rebuilt on
+ * `rebuild` in the run's own precision (bench.hpp:363-382); both plans hold the same data. */
+GPEMU_API int gpemu_refine_fit_ex(gpemu_plan* polish, gpemu_plan* rebuild, const double* lo,
+                                  const double* hi, const double* theta_fit, double neg2_fit,
+                                  int budget, double* theta_out, double* neg2_out, int* evals_out,
+                                  gpemu_model** model_out, double* scalars, double* alpha);
 
 /* model_at_theta (likelihood.hpp:216-237). scalars: neg2, mu, sigma2, jitter. */
 GPEMU_API int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,

@@ -93,10 +93,14 @@ struct ProfileEval {
 class BatchEvaluator {
  public:
   // X: n x d row-major on the unit cube, y: n outputs.
+  // precision: GPEMU_PRECISION_DOUBLE, or GPEMU_PRECISION_SINGLE for the reference's float
+  // instantiation (Precision::kSingle, core.hpp:86-96).
   BatchEvaluator(Context& ctx, std::span<const double> X, std::span<const double> y, std::size_t d,
-                 double p, double nugget, std::size_t max_batch)
+                 double p, double nugget, std::size_t max_batch,
+                 int precision = GPEMU_PRECISION_DOUBLE)
       : d_(d), n_(y.size()) {
-    check(gpemu_plan_create(ctx.get(), X.data(), y.data(), n_, d_, p, nugget, max_batch, &h_));
+    check(gpemu_plan_create_ex(ctx.get(), X.data(), y.data(), n_, d_, p, nugget, max_batch,
+                               precision, &h_));
   }
   ~BatchEvaluator() { gpemu_plan_destroy(h_); }
   BatchEvaluator(const BatchEvaluator&) = delete;
@@ -194,14 +198,19 @@ inline FitResult fit_gp_detailed(BatchEvaluator& ev, std::span<const double> lo,
 // The bench protocol's post-GA polish (bench.hpp:302-383 detail::refine_fit): `budget`
 // golden-section evaluations around fit.theta; fit (theta, scalars, alpha, model) is replaced
 // when -2logL improves. Returns the extra evaluations (budget, +1 for the model rebuild).
+// `polish` (optional): a double-precision evaluator on the same data for the polish itself,
+// as the reference polishes in double regardless of the run precision (bench.hpp:300-301);
+// the model is rebuilt on `ev` (the run's precision).
 inline std::size_t refine_fit(BatchEvaluator& ev, FitResult& fit, std::span<const double> lo,
-                              std::span<const double> hi, int budget = 20) {
+                              std::span<const double> hi, int budget = 20,
+                              BatchEvaluator* polish = nullptr) {
   std::vector<double> theta(ev.d()), alpha(ev.n());
   double neg2 = 0.0, sc[4] = {};
   int used = 0;
   gpemu_model* m = nullptr;
-  check(gpemu_refine_fit(ev.get(), lo.data(), hi.data(), fit.theta.data(), fit.neg2_log_lik,
-                         budget, theta.data(), &neg2, &used, &m, sc, alpha.data()));
+  check(gpemu_refine_fit_ex(polish ? polish->get() : ev.get(), ev.get(), lo.data(), hi.data(),
+                            fit.theta.data(), fit.neg2_log_lik, budget, theta.data(), &neg2, &used,
+                            &m, sc, alpha.data()));
   if (!m) return static_cast<std::size_t>(used);
   fit.model = Model(m);
   fit.theta = std::move(theta);

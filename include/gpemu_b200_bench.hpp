@@ -9,8 +9,9 @@
 //   fit_gp_detailed -> gpemu_fit, refine_fit -> gpemu_refine_fit, predict -> gpemu_predict.
 // "reference" / "parallel" cells are the reference's own run_bench_cell, unchanged.
 //
-// Requires the reference headers (gpemu/gpemu.hpp) to be included first; the accelerated
-// path is double-only: precision=single with "accelerated" is a ConfigError.
+// Requires the reference headers (gpemu/gpemu.hpp) to be included first. precision=single
+// runs the accelerated cells on the FP32 engine (GPEMU_PRECISION_SINGLE) with the polish in
+// double, as the reference does.
 #pragma once
 
 #ifndef GPEMU_REFERENCE_PLUGIN
@@ -36,8 +37,7 @@ inline gpemu::BenchReportRow run_bench_cell_accelerated(Context& ctx, const gpem
   row.precision = std::string(gpemu::precision_name(cfg.precision));
   row.n = n;
   row.replication = rep;
-  if (cfg.precision != gpemu::Precision::kDouble)
-    throw gpemu::ConfigError("bench: the accelerated backend is double precision only");
+  const bool single = cfg.precision == gpemu::Precision::kSingle;
 
   GaConfig ga;
   ga.population = cfg.ga_population;
@@ -52,10 +52,19 @@ inline gpemu::BenchReportRow run_bench_cell_accelerated(Context& ctx, const gpem
   try {
     const auto t0 = std::chrono::steady_clock::now();
     const auto& X = data.inputs();
-    BatchEvaluator ev(ctx, std::span<const double>(X.data(), X.rows() * X.cols()), data.outputs(),
-                      data.d(), kP, 0.0, static_cast<std::size_t>(ga.population));
+    const std::span<const double> Xs(X.data(), X.rows() * X.cols());
+    BatchEvaluator ev(ctx, Xs, data.outputs(), data.d(), kP, 0.0,
+                      static_cast<std::size_t>(ga.population),
+                      single ? GPEMU_PRECISION_SINGLE : GPEMU_PRECISION_DOUBLE);
     FitResult fit = fit_gp_detailed(ev, lo, hi, ga, seed);
-    if (cfg.refine) row.eval_count += refine_fit(ev, fit, lo, hi, 20);
+    if (cfg.refine) {
+      if (single) {  // the polish runs in double whatever the run precision (bench.hpp:300)
+        BatchEvaluator polish(ctx, Xs, data.outputs(), data.d(), kP, 0.0, 1);
+        row.eval_count += refine_fit(ev, fit, lo, hi, 20, &polish);
+      } else {
+        row.eval_count += refine_fit(ev, fit, lo, hi, 20);
+      }
+    }
     const auto predictions = predict(
         fit.model, std::span<const double>(test_inputs.data(), test_inputs.rows() * test_inputs.cols()),
         test_inputs.cols());
@@ -128,7 +137,7 @@ inline std::vector<gpemu::BenchReportRow> run_bench(const gpemu::BenchConfig& cf
       for (const auto& backend_id : cfg.backends) {
         if (backend_id == "accelerated") {
           emit(run_bench_cell_accelerated(*ctx, cfg, data, test_inputs, truth, n, rep));
-        } else if (cfg.precision == gpemu::Precision::kSingle) {
+        } else if (cfg.precision == gpemu::Precision::kSingle) {  // the reference's float cells
           emit(gpemu::detail::run_bench_cell<float>(cfg, data, test_inputs, truth, backend_id, n, rep));
         } else {
           emit(gpemu::detail::run_bench_cell<double>(cfg, data, test_inputs, truth, backend_id, n, rep));

@@ -1119,7 +1119,21 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
 int gpemu_refine_fit(gpemu_plan* pl, const double* lo, const double* hi, const double* theta_fit,
                      double neg2_fit, int budget, double* theta_out, double* neg2_out,
                      int* evals_out, gpemu_model** model_out, double* scalars, double* alpha) {
+  return gpemu_refine_fit_ex(pl, pl, lo, hi, theta_fit, neg2_fit, budget, theta_out, neg2_out,
+                             evals_out, model_out, scalars, alpha);
+}
+
+// bench.hpp:302-383 with the polish evaluations on `pl` (double precision regardless of the
+// run precision, bench.hpp:300-301) and the model rebuilt on `rebuild` in the run's own
+// precision (bench.hpp:363-382).
+int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, const double* hi,
+                        const double* theta_fit, double neg2_fit, int budget, double* theta_out,
+                        double* neg2_out, int* evals_out, gpemu_model** model_out, double* scalars,
+                        double* alpha) {
   GPEMU_GUARD_BEGIN
+  if (!rebuild) rebuild = pl;
+  if (!pl || pl->d != rebuild->d || pl->n != rebuild->n)
+    return set_error(GPEMU_VALIDATION, "refine_fit: polish and rebuild plans must share the dataset");
   if (!pl || !lo || !hi || !theta_fit) return set_error(GPEMU_VALIDATION, "refine_fit: null argument");
   const int d = pl->d;
   for (int k = 0; k < d; ++k)
@@ -1187,12 +1201,14 @@ int gpemu_refine_fit(gpemu_plan* pl, const double* lo, const double* hi, const d
   if (model_out) {
     *model_out = nullptr;
     if (best_value < neg2_fit) {
-      ck(cudaMemcpyAsync(pl->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
-      rc = run_batch(pl, 1);
+      gpemu_plan* rb = rebuild;
+      ck(cudaMemcpyAsync(rb->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice,
+                         rb->ctx->stream), "H2D theta");
+      rc = run_batch(rb, 1);
       if (rc) return rc;
-      download_records(pl, 1);
-      if (std::isfinite(pl->h_out[REC_NEG2]) && pl->h_out[REC_NEG2] < neg2_fit) {
-        gpemu_model* m = make_model(pl, 0, theta.data(), pl->h_out.data());
+      download_records(rb, 1);
+      if (std::isfinite(rb->h_out[REC_NEG2]) && rb->h_out[REC_NEG2] < neg2_fit) {
+        gpemu_model* m = make_model(rb, 0, theta.data(), rb->h_out.data());
         if (scalars) {
           scalars[0] = m->neg2;
           scalars[1] = m->mu;

@@ -75,7 +75,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
-    "gpemu_plan_create_ex", "gpemu_plan_precision",
+    "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex",
 )
 
 
@@ -141,6 +141,8 @@ def lib():
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]
     L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
+    L.gpemu_refine_fit_ex.argtypes = [_vp, _vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
+                                      C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_destroy.argtypes = [_vp]
     L.gpemu_predict.argtypes = [_vp, _dp, _sz, _dp, _dp]
     _LIB = L
@@ -749,15 +751,20 @@ def refine_fit(fit: FitResult, data: Dataset, cfg: FitConfig, backend: Backend,
     bounds = cfg.bounds_for(d)
     lo = _f64([b[0] for b in bounds])
     hi = _f64([b[1] for b in bounds])
+    # the polish evaluates in double whatever the run precision (bench.hpp:300-301); the model
+    # is rebuilt in the run's precision (bench.hpp:363-382)
     ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=1)
+    rb = ev if parse_precision(cfg.precision) == "double" else ProfileEvaluator(
+        data, cfg.p, cfg.nugget, backend, max_batch=1, precision=cfg.precision)
     try:
         th = np.empty(d)
         sc = np.empty(4)
         alpha = np.empty(data.n())
         nv, used, mh = C.c_double(), C.c_int(), _vp()
-        _check(lib().gpemu_refine_fit(ev.handle, _p(lo), _p(hi), _p(_f64(fit.model.params.theta)),
-                                      float(fit.model.neg2_log_lik), int(budget), _p(th),
-                                      C.byref(nv), C.byref(used), C.byref(mh), _p(sc), _p(alpha)))
+        _check(lib().gpemu_refine_fit_ex(ev.handle, rb.handle, _p(lo), _p(hi),
+                                         _p(_f64(fit.model.params.theta)),
+                                         float(fit.model.neg2_log_lik), int(budget), _p(th),
+                                         C.byref(nv), C.byref(used), C.byref(mh), _p(sc), _p(alpha)))
         extra = used.value
         if mh.value:
             extra += 1
@@ -771,6 +778,8 @@ def refine_fit(fit: FitResult, data: Dataset, cfg: FitConfig, backend: Backend,
         return extra
     finally:
         ev.close()
+        if rb is not ev:
+            rb.close()
 
 
 def fit_gp(data: Dataset, cfg: FitConfig, backend: Backend) -> GpModel:

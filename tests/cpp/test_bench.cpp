@@ -71,18 +71,25 @@ int main(int argc, char** argv) {
   }
   const auto summary = summarize(rows);
   CHECK(!summary.empty());
-  {  // single precision + accelerated is a configuration error, like an unknown backend
-    BenchConfig bad = cfg;
-    bad.precision = Precision::kSingle;
-    bad.backends = {"accelerated"};
-    bad.output_path.clear();
-    bool threw = false;
-    try {
-      gpemu_b200::run_bench(bad);
-    } catch (const ConfigError&) {
-      threw = true;
+  {  // precision = single: accelerated cells on the FP32 engine (polish in double) next to the
+     // reference's float cells. Float GA trajectories may diverge (fitness noise ~1e-3), so the
+     // rows are checked structurally and for a deviance of the same magnitude.
+    BenchConfig sc = cfg;
+    sc.precision = Precision::kSingle;
+    sc.backends = {"parallel", "accelerated"};
+    sc.sizes = {60};
+    sc.output_path.clear();
+    const auto srows = gpemu_b200::run_bench(sc, &std::cout);
+    CHECK(srows.size() == 2 * 1 * 2);
+    for (std::size_t i = 0; i + 1 < srows.size(); i += 2) {
+      const auto &r = srows[i], &a = srows[i + 1];
+      CHECK(a.precision == "single" && r.precision == "single");
+      CHECK(!a.failed && !r.failed);
+      CHECK(a.eval_count >= 24 * 6 + 20 && a.eval_count <= 24 * 6 + 21);
+      CHECK(std::abs(a.neg2_log_lik - r.neg2_log_lik) <= 0.1 * std::abs(r.neg2_log_lik));
+      std::printf("single n=%zu rep=%d neg2 ref %.6g acc %.6g\n", a.n, a.replication, r.neg2_log_lik,
+                  a.neg2_log_lik);
     }
-    CHECK(threw);
   }
   std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASSED", failures);
   return failures ? 1 : 0;
