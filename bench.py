@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-single", action="store_true",
+                    help="skip the informational single-precision (FP32 engine) rate")
     ap.add_argument("--cpu-sample", type=int, default=0, help="evals in the CPU sample (0: auto)")
     return ap.parse_args()
 
@@ -348,6 +350,26 @@ def main():
         "e2e": r["e2e"],
         "candidates_ok": r["status_ok"],
     }
+    # ---- informational: the same batches on the single-precision engine (Precision::kSingle) ----
+    if rank == 0 and world == 1 and not args.no_single:
+        import torch
+        import paper_1203_1269_b200.gpemu as g
+        evs = g.ProfileEvaluator(g.new_dataset(r["X"], r["y"]), args.p, 0.0, r["be"],
+                                 max_batch=B, precision="single")
+        for b in r["batches"][:2]:
+            evs.eval_batch(b)
+        evs.set_profiling(True)
+        t0 = time.time()
+        for s in range(args.steps):
+            evs.eval_batch(r["batches"][s % len(r["batches"])])
+        wall = time.time() - t0
+        sc_ms, _ = evs.phase_ms(1)
+        evs.set_profiling(False)
+        line["single_precision"] = {
+            "value": B * args.steps / wall, "unit": UNIT, "chol_ms_per_step": sc_ms / args.steps,
+            "note": "informational: FP32 engine (float R/factor/solves, dots in double) on the same "
+                    "batches, host-timed through eval_batch; the headline value is FP64"}
+        evs.close()
     # ---- fit wall time (GA 100 x 20 on the same design) ----
     if rank == 0 and world == 1 and not args.no_fit:
         import paper_1203_1269_b200.gpemu as g
