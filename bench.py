@@ -169,8 +169,7 @@ def run_reference_arm(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"C3 n={args.n} d={args.d} p={args.p}", "n": args.n, "d": args.d,
-                   "p": args.p, "batch_per_gpu": args.batch},
+        "config": bench_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
                          "sample": f"{per_step} evals per step x {args.steps} steps of the step-0 "
                                    f"theta batch; ParallelBackend(hardware_concurrency); "
@@ -178,6 +177,18 @@ def run_reference_arm(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     return line
+
+
+def bench_config(args, world):
+    """The workload description both arms print (the reference arm runs the same config)."""
+    n, B = args.n, args.batch
+    return {"workload": f"C3: n={n}, d={args.d}, p={args.p}; {B} theta candidates per GPU "
+                        "per step (one GA generation); random LHD design, smooth_response y, "
+                        "thetas from the GA's LHS over the log10 box [1e-6, 12]^d",
+            "n": n, "d": args.d, "p": args.p, "batch_per_gpu": B, "global_batch": B * world,
+            "parallelism": f"candidate sharding x{world} (weak)",
+            "l2": "inputs larger than L2 (per-step working set ~%.1f GB)" % (
+                B * (n / 128) * (n / 128 + 1) / 2 * 128 * 128 * 8 / 1e9)}
 
 
 # ----------------------------------------------------------------- our arm
@@ -329,13 +340,7 @@ def main():
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"C3: n={n}, d={args.d}, p={args.p}; {B} theta candidates per GPU "
-                               "per step (one GA generation); random LHD design, smooth_response y, "
-                               "thetas from the GA's LHS over the log10 box [1e-6, 12]^d",
-                   "n": n, "d": args.d, "p": args.p, "batch_per_gpu": B, "global_batch": B * world,
-                   "parallelism": f"candidate sharding x{world} (weak)",
-                   "l2": "inputs larger than L2 (per-step working set ~%.1f GB)" % (
-                       B * (n / 128) * (n / 128 + 1) / 2 * 128 * 128 * 8 / 1e9)},
+        "config": bench_config(args, world),
         "roofline": {"kernel": "chol_dag_kernel", "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                      "peak_source": peak_src + " (FP64: MEASURED_PEAKS.json has bf16/HBM only)",
