@@ -584,12 +584,18 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // operand, free in DMMA): the running-residual order of the reference's
       // `v -= L_it * L_jt` (backend.hpp:197-204), which keeps the rounding error
       // relative to the shrinking residual instead of the growing sum.
+      // Row ownership: OFF tasks give warp w rows 16w..16w+15 (the TRSM needs whole rows per
+      // warp). DIAG tasks only need the lower triangle, so warp w takes the 8-row m-tiles w
+      // and 15 - w instead: every warp then computes 17 of the 32 n-tile products per k-step
+      // (the upper triangle is skipped, balanced across warps).
+      const int rowA = diag ? 8 * warp + lr : 16 * warp + lr;
+      const int rowB = diag ? 8 * (15 - warp) + lr : 16 * warp + 8 + lr;
       double acc[2][16][2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 16; ++ni) {
-          const int off = acc_off(16 * warp + 8 * mi + lr, ni, lc);
+          const int off = acc_off(mi ? rowB : rowA, ni, lc);
           const double2 v = skip ? make_double2(0.0, 0.0)
                                  : __ldcg(reinterpret_cast<const double2*>(gtile + off));
           acc[mi][ni][0] = v.x;
@@ -646,17 +652,35 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
         const double* As = reinterpret_cast<const double*>(smem + kOffStages + stage * kStageBytes);
         const double* Bs = diag ? As : As + SLAB_ELEMS;
-        const double* Aw = As + (16 * warp + lr) * 32 + lc;
         const double* Bw = Bs + lr * 32 + lc;
+        if (!diag) {
+          const double* Aw = As + (16 * warp + lr) * 32 + lc;
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const int ko = (ks ^ lr) << 2;
-          const double a0 = -Aw[ko], a1 = -Aw[256 + ko];
+          for (int ks = 0; ks < 8; ++ks) {
+            const int ko = (ks ^ lr) << 2;
+            const double a0 = -Aw[ko], a1 = -Aw[256 + ko];
 #pragma unroll
-          for (int ni = 0; ni < 16; ++ni) {
-            const double b = Bw[ni * 256 + ko];
-            dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
-            dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
+            for (int ni = 0; ni < 16; ++ni) {
+              const double b = Bw[ni * 256 + ko];
+              dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
+              dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
+            }
+          }
+        } else {  // lower triangle only: m-tile w needs n-tiles 0..w, m-tile 15-w 0..15-w
+          const double* Aw0 = As + rowA * 32 + lc;
+          const double* Aw1 = As + rowB * 32 + lc;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int ko = (ks ^ lr) << 2;
+            const double a0 = -Aw0[ko], a1 = -Aw1[ko];
+#pragma unroll
+            for (int ni = 0; ni < 16; ++ni) {
+              if (ni <= warp || ni <= 15 - warp) {
+                const double b = Bw[ni * 256 + ko];
+                if (ni <= warp) dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
+                if (ni <= 15 - warp) dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
+              }
+            }
           }
         }
         if (diag) {
@@ -696,7 +720,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
           for (int ni = 0; ni < 16; ++ni)
-            *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, ni, lc)) =
+            *reinterpret_cast<double2*>(C + acc_off(mi ? rowB : rowA, ni, lc)) =
                 make_double2(acc[mi][ni][0], acc[mi][ni][1]);
         consumer_sync();
         if (tid == 0) pr.lap(PR_ACC_STORE);
