@@ -41,6 +41,9 @@ def test_library_is_sm100a(g):
     sec = sass.split("chol_dag_kernel", 1)[1].split("Function :", 1)[0]
     # FP64 tensor-core tiles (DMMA) fed by bulk (TMA) copies completing on mbarriers
     assert "DMMA.8x8x4" in sec and "UBLKCP" in sec and "SYNCS.ARRIVE.TRANS64" in sec
+    # the single-precision engine: FFMA tiles fed by the same bulk copies
+    sec32 = sass.split("chol_dag_f32_kernel", 1)[1].split("Function :", 1)[0]
+    assert "FFMA" in sec32 and "UBLKCP" in sec32 and "DMMA" not in sec32
 
 
 def test_no_gpu_fails_loudly(g):
