@@ -199,6 +199,9 @@ GPEMU_API int gpemu_refine_fit_ex(gpemu_plan* polish, gpemu_plan* rebuild, const
 /* model_at_theta (likelihood.hpp:216-237). scalars: neg2, mu, sigma2, jitter. */
 GPEMU_API int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_model** model_out,
                          double* scalars, double* alpha);
+/* A model's scalars: out[4] = {neg2_log_lik, mu_hat, sigma2_hat, jitter_used}
+ * (GpModel fields, likelihood.hpp:171-182; factor.jitter_used, backend.hpp:54-70). */
+GPEMU_API int gpemu_model_scalars(const gpemu_model* model, double* out);
 GPEMU_API int gpemu_model_destroy(gpemu_model* model);
 
 /* ---- predictor.hpp ------------------------------------------------------ */

@@ -1253,6 +1253,15 @@ int gpemu_model_at_theta(gpemu_plan* pl, const double* theta, gpemu_model** mode
   GPEMU_GUARD_END
 }
 
+int gpemu_model_scalars(const gpemu_model* m, double* out) {
+  if (!m || !out) return set_error(GPEMU_VALIDATION, "model_scalars: null argument");
+  out[0] = m->neg2;
+  out[1] = m->mu;
+  out[2] = m->sigma2;
+  out[3] = m->jitter;
+  return GPEMU_OK;
+}
+
 int gpemu_model_destroy(gpemu_model* m) {
   delete m;
   return GPEMU_OK;

@@ -75,7 +75,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_model_destroy", "gpemu_predict", "gpemu_plan_set_profiling", "gpemu_plan_phase_ms",
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
-    "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex",
+    "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
 )
 
 
@@ -141,6 +141,7 @@ def lib():
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]
     L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
+    L.gpemu_model_scalars.argtypes = [_vp, _dp]
     L.gpemu_refine_fit_ex.argtypes = [_vp, _vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                       C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_destroy.argtypes = [_vp]
@@ -470,8 +471,25 @@ class Backend:
     def solve_full(self, f: CorrelationFactor, b) -> np.ndarray:
         return self.solve_upper(f, self.solve_lower(f, b))
 
+    # the reference's in-place forms (backend.hpp:102, :129, :143)
+    def factorize_into(self, R: CorrelationMatrix, out: CorrelationFactor) -> None:
+        f = self.factorize(R)
+        out.lower, out.log_det, out.jitter_used = f.lower, f.log_det, f.jitter_used
+
+    def solve_lower_into(self, f: CorrelationFactor, b, x: np.ndarray) -> None:
+        x[...] = self.solve_lower(f, b)
+
+    def solve_upper_into(self, f: CorrelationFactor, b, x: np.ndarray) -> None:
+        x[...] = self.solve_upper(f, b)
+
 
 _REGISTRY = {"accelerated": lambda threads=0: Backend()}
+
+
+def backend_registry() -> dict:
+    """backend.hpp:324-331. This package registers only "accelerated"; the reference's
+    "reference" / "parallel" CPU backends are the oracle (oracle/), not part of the product."""
+    return _REGISTRY
 
 
 def make_backend(id: str, threads: int = 0) -> Backend:
@@ -494,6 +512,43 @@ class ProfileEval:
     mu_hat: float = 0.0
     sigma2_hat: float = 0.0
     jitter_used: float = 0.0
+
+
+def _dot_accumulate(a, b) -> float:
+    """matrix.hpp:64-69: sequential double dot."""
+    s = 0.0
+    for x, z in zip(np.asarray(a, dtype=np.float64).tolist(), np.asarray(b, dtype=np.float64).tolist()):
+        s += x * z
+    return s
+
+
+def mu_hat(backend: Backend, f: CorrelationFactor, y) -> float:
+    """likelihood.hpp:32-44: (v.u)/(v.v), u = L^-1 y, v = L^-1 1 (two solves)."""
+    y = _f64(y)
+    if y.shape[0] != f.n():
+        raise ValidationError("mu_hat: output length mismatch")
+    u = backend.solve_lower(f, y)
+    v = backend.solve_lower(f, np.ones_like(y))
+    vtv = _dot_accumulate(v, v)
+    if not vtv > 0.0:
+        raise Error("mu_hat: degenerate denominator (broken factor)")
+    return _dot_accumulate(v, u) / vtv
+
+
+def sigma2_hat(backend: Backend, f: CorrelationFactor, y, mu: float) -> float:
+    """likelihood.hpp:47-57: (y - mu)' R^-1 (y - mu) / n via one solve."""
+    y = _f64(y)
+    if y.shape[0] != f.n():
+        raise ValidationError("sigma2_hat: output length mismatch")
+    w = backend.solve_lower(f, y - mu)
+    s = _dot_accumulate(w, w) / y.shape[0]
+    return 0.0 if s < 0.0 else s
+
+
+def sigma2_hat_from_parts(utu: float, vtu: float, vtv: float, mu: float, n: int) -> float:
+    """likelihood.hpp:63-66: w'w = u'u - 2 mu v'u + mu^2 v'v, floored at 0."""
+    s = (utu - 2.0 * mu * vtu + mu * mu * vtv) / float(n)
+    return 0.0 if s < 0.0 else s
 
 
 class ProfileEvaluator:
@@ -627,6 +682,13 @@ class GpModel:
         self.neg2_log_lik = neg2
         self.alpha = alpha
         self.ctx = ctx
+
+    @property
+    def jitter_used(self) -> float:
+        """factor.jitter_used of the model's factorization (backend.hpp:54-70)."""
+        sc = np.empty(4)
+        _check(lib().gpemu_model_scalars(self.handle, _p(sc)))
+        return float(sc[3])
 
     def close(self):
         if getattr(self, "handle", None):
@@ -817,6 +879,36 @@ def predict(model: GpModel, test_inputs, with_mse: bool = False):
     mse = np.empty(N) if with_mse else None
     _check(lib().gpemu_predict(model.handle, _p(Xt), N, _p(yhat), _p(mse)))
     return (yhat, mse) if with_mse else yhat
+
+
+def model_alpha_residual(model: GpModel) -> float:
+    """likelihood.hpp:191-213: ||(R + jitter I) alpha - (y - 1 mu)||_inf / ||y||_inf with R rebuilt
+    from the stored hyperparameters (the GpModel contract keeps it <= 1e-6 in double)."""
+    X = model.dataset.inputs()
+    R = build_corr_matrix(X, model.params, model.ctx).values.copy()
+    R[np.diag_indices_from(R)] += model.jitter_used
+    y = model.dataset.outputs()
+    row = R @ _f64(model.alpha)
+    worst = float(np.max(np.abs(row - (y - model.mu_hat))))
+    ymax = float(np.max(np.abs(y)))
+    return worst / ymax if ymax > 0.0 else worst
+
+
+@dataclass
+class PredictionSet:
+    """predictor.hpp:64-69."""
+    test_inputs: np.ndarray
+    predictions: np.ndarray
+    sspe: float = 0.0
+
+
+def predict_set(model: GpModel, test_inputs, truth=None) -> PredictionSet:
+    """predictor.hpp:71-79: predictions plus, when truth is given, their SSPE."""
+    Xt = _f64(test_inputs)
+    out = PredictionSet(Xt, predict(model, Xt))
+    if truth is not None and len(truth):
+        out.sspe = sspe(out.predictions, truth)
+    return out
 
 
 def sspe(predictions, truth) -> float:

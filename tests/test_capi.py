@@ -96,3 +96,14 @@ def test_sspe(g):
     assert g.sspe([1.0, 2.0], [1.5, 1.0]) == 1.25
     with pytest.raises(g.ValidationError):
         g.sspe([1.0], [1.0, 2.0])
+
+
+def test_host_side_reference_names(g):
+    """likelihood.hpp:63-66 sigma2_hat_from_parts and the backend registry (backend.hpp:324-351)."""
+    assert g.sigma2_hat_from_parts(4.0, 1.0, 2.0, 0.5, 2) == (4.0 - 1.0 + 0.5) / 2
+    assert g.sigma2_hat_from_parts(0.0, 1.0, 0.0, 1.0, 3) == 0.0  # floored at zero
+    assert "accelerated" in g.backend_registry()
+    with pytest.raises(g.ConfigError):
+        g.make_backend("parallel")  # the CPU backends are the oracle, not the product
+    with pytest.raises(g.ConfigError):
+        g.FitConfig(precision="half") and g.parse_precision("half")

@@ -451,3 +451,32 @@ def test_single_precision_fit(g, ctx, ref_fast):
     assert fr.ledger.factorizations == 100
     yhat = g.predict(fr.model, X[:20])  # the float model interpolates its design
     assert np.max(np.abs(yhat - y[:20])) <= 1e-2 * np.abs(y).max()
+
+
+def test_reference_helpers_on_device(g, ctx):
+    """mu_hat / sigma2_hat (likelihood.hpp:32-57) through the device solves agree with the batched
+    evaluation record; the *_into forms; model_alpha_residual <= 1e-6 (the GpModel contract,
+    likelihood.hpp:191-213); predict_set (predictor.hpp:71-79)."""
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    X, y = z["X"], z["y"]
+    th = np.array([3.0, 2.0])
+    be = g.Backend(ctx)
+    data = g.new_dataset(X, y)
+    R = g.build_corr_matrix(X, g.Hyperparameters(th, 1.95), ctx)
+    f = g.CorrelationFactor(np.empty((0, 0)))
+    be.factorize_into(R, f)
+    mu = g.mu_hat(be, f, y)
+    s2 = g.sigma2_hat(be, f, y, mu)
+    ev = g.ProfileEvaluator(data, 1.95, 0.0, be, max_batch=1)
+    rec = ev.eval_batch(th[None, :])
+    assert rel(mu, rec["mu"][0]) <= 1e-9 and rel(s2, rec["sigma2"][0]) <= 1e-8
+    x = np.empty(len(y))
+    be.solve_lower_into(f, y, x)
+    assert np.allclose(np.tril(f.lower) @ x, y, rtol=0, atol=1e-8 * np.abs(y).max())
+    m = g.model_at_theta(data, th, 1.95, 0.0, be)
+    assert m.jitter_used == rec["jitter"][0]
+    assert g.model_alpha_residual(m) <= 1e-6
+    ps = g.predict_set(m, z["Xt"][:50], truth=np.zeros(50))
+    assert ps.predictions.shape == (50,) and ps.sspe == g.sspe(ps.predictions, np.zeros(50))
+    ev.close()
+    m.close()
