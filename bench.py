@@ -192,9 +192,30 @@ def bench_config(args, world):
 
 
 # ----------------------------------------------------------------- our arm
+# Collectives backend for the multi-rank path: NCCL (one rank per GPU, the contract). The
+# test-only override GPEMU_BENCH_DIST=gloo runs the same host logic with CPU collectives and
+# maps ranks onto the visible GPUs, so the world > 1 code path can be exercised on one GPU
+# (ranks never wait on each other's kernels: the work is independent candidate batches).
+DIST_BACKEND = os.environ.get("GPEMU_BENCH_DIST", "nccl")
+
+
+def rank_device(local_rank):
+    import torch
+    return local_rank if DIST_BACKEND == "nccl" else local_rank % max(1, torch.cuda.device_count())
+
+
+def max_over_ranks(x, dev):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=dev if DIST_BACKEND == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1203_1269_b200.gpemu as g
+    local_rank = rank_device(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     X, y, batches = make_inputs(args, rank)
@@ -239,11 +260,7 @@ def run_ours(args, rank, world, local_rank):
     ev.set_profiling(False)
     rec = d_out.view(B, 8).cpu().numpy()
     status = rec[:, 5]
-    ms_max = ms
-    if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, dev) if dist is not None else ms
     value = world * B * args.steps / (ms_max / 1e3)
 
     # ---- e2e: the public API with pinned host buffers (H2D thetas, D2H records) ----
@@ -275,9 +292,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize(dev)
         ems = f0.elapsed_time(f1)
         if dist is not None:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = max_over_ranks(ems, dev)
         e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": B * args.d * 8, "d2h_bytes_per_step": B * (5 * 8 + 4),
                "api": "gpemu_eval_batch (C-ABI, host buffers)"}
@@ -326,8 +341,11 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if DIST_BACKEND == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(DIST_BACKEND)
 
     r = run_ours(args, rank, world, local_rank)
     B, n = args.batch, args.n

@@ -50,3 +50,35 @@ def test_sharded_fit_under_torchrun_nccl():
     r = _torchrun(["tools/sharded_fit.py", "512", "3", "16", "3"])
     assert r.returncode == 0, r.stderr[-3000:]
     assert "sharded fit n=512" in r.stdout
+
+
+def _torchrun_n(n, args, env_extra, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(_port())] + args
+    env = dict(os.environ, **env_extra)
+    return subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT, env=env)
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_host_logic():
+    """bench.py with world 2 (barriers, max-over-ranks time, rank-0 line, weak-scaling value):
+    collectives on gloo and both ranks on the visible GPU (GPEMU_BENCH_DIST=gloo, test-only),
+    since this pool gives one GPU; the ranks' batches are independent."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    r = _torchrun_n(2, ["bench.py", "--gpus", "2", "--steps", "3", "--warmup", "3", "--size", "768",
+                        "--dims", "3", "--batch", "16", "--no-fit", "--no-cpu-baseline", "--no-single"],
+                    {"GPEMU_BENCH_DIST": "gloo"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1  # rank 0 only
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 32
+    assert abs(line["value"] - 2 * 16 * 3 / (line["ms_per_step"] * 3 / 1e3)) <= 1e-6 * line["value"]
+    assert line["e2e"]["value"] > 0
+    r = _torchrun_n(2, ["bench.py", "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                        "--size", "768", "--dims", "3", "--batch", "16"], {"GPEMU_BENCH_DIST": "gloo"})
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and json.loads(lines[0])["impl"] == "reference"
