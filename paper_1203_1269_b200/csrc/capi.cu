@@ -135,6 +135,11 @@ struct gpemu_ctx {
   int engine = GPEMU_ENGINE_DAG;
   int num_sms = 148;
   uint64_t launches = 0;
+  // Backend-level single-matrix calls (try_cholesky / factorize): a one-slot plan and an n x n
+  // staging matrix reused across calls (the reference's fit through the plugin makes
+  // thousands of them), rebuilt only when n changes.
+  gpemu_plan* scratch = nullptr;
+  DevBuf<double> scratch_a, scratch_l;
 };
 
 struct gpemu_plan {
@@ -430,6 +435,7 @@ int gpemu_ctx_create(int device, gpemu_ctx** out) {
 
 int gpemu_ctx_destroy(gpemu_ctx* ctx) {
   if (!ctx) return GPEMU_OK;
+  delete ctx->scratch;
   if (ctx->own) cudaStreamDestroy(ctx->own);
   delete ctx;
   return GPEMU_OK;
@@ -553,15 +559,31 @@ static void single_slot_plan(gpemu_ctx* ctx, gpemu_plan& pl, size_t n) {
   ck(cudaMemsetAsync(pl.error.p, 0, sizeof(int), s), "memset");
 }
 
+// The context's reusable one-slot plan for n (see gpemu_ctx::scratch).
+static gpemu_plan& scratch_plan(gpemu_ctx* ctx, size_t n) {
+  if (!ctx->scratch || ctx->scratch->n != (int)n) {
+    delete ctx->scratch;
+    ctx->scratch = nullptr;
+    auto* pl = new gpemu_plan();
+    try {
+      single_slot_plan(ctx, *pl, n);
+    } catch (...) {
+      delete pl;
+      throw;
+    }
+    ctx->scratch = pl;
+  }
+  return *ctx->scratch;
+}
+
 int gpemu_try_cholesky(gpemu_ctx* ctx, double* A, size_t n) {
   GPEMU_GUARD_BEGIN
   if (!ctx || !A || n == 0) return set_error(GPEMU_VALIDATION, "try_cholesky: bad argument");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-  gpemu_plan pl;
-  single_slot_plan(ctx, pl, n);
+  gpemu_plan& pl = scratch_plan(ctx, n);
   cudaStream_t s = ctx->stream;
-  DevBuf<double> dA;
-  dA.alloc(n * n);
+  DevBuf<double>& dA = ctx->scratch_a;
+  dA.reserve(n * n);
   ck(cudaMemcpyAsync(dA.p, A, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D A");
   int st = 0;
   double rec[REC_SIZE];
@@ -582,11 +604,10 @@ int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, do
   GPEMU_GUARD_BEGIN
   if (!ctx || !R || n == 0) return set_error(GPEMU_VALIDATION, "factorize: bad argument");
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
-  gpemu_plan pl;
-  single_slot_plan(ctx, pl, n);
+  gpemu_plan& pl = scratch_plan(ctx, n);
   cudaStream_t s = ctx->stream;
-  DevBuf<double> dR;
-  dR.alloc(n * n);
+  DevBuf<double>& dR = ctx->scratch_a;
+  dR.reserve(n * n);
   ck(cudaMemcpyAsync(dR.p, R, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D R");
   for (int step = 0; step < 6; ++step) {
     const double jit = kLadder[step];
@@ -596,8 +617,8 @@ int gpemu_factorize(gpemu_ctx* ctx, const double* R, size_t n, double* L_out, do
     if (rc) return rc;
     if (st == 0) {
       if (L_out) {
-        DevBuf<double> dL;
-        dL.alloc(n * n);
+        DevBuf<double>& dL = ctx->scratch_l;
+        dL.reserve(n * n);
         launch_tiles_to_rowmajor(pl.factors.p, pl.n, pl.NT, dL.p, s);
         ctx->launches += 1;
         ck(cudaMemcpyAsync(L_out, dL.p, n * n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
