@@ -480,3 +480,32 @@ def test_reference_helpers_on_device(g, ctx):
     assert ps.predictions.shape == (50,) and ps.sspe == g.sspe(ps.predictions, np.zeros(50))
     ev.close()
     m.close()
+
+
+def test_concurrent_contexts_in_threads(g):
+    """Distinct contexts used concurrently from distinct host threads (the reference's concurrent
+    replications, bench.hpp:503-516) give the same records as sequential use."""
+    import threading
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    X, y, th = z["X"], z["y"], z["thetas"][:16]
+    seq = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(g.Context(0)),
+                             max_batch=16).eval_batch(th)
+    out, errs = [None] * 4, []
+
+    def work(i):
+        try:
+            ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(g.Context(0)), max_batch=16)
+            for _ in range(3):
+                out[i] = ev.eval_batch(th)
+            ev.close()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t_ in ts:
+        t_.start()
+    for t_ in ts:
+        t_.join()
+    assert not errs, errs
+    for r in out:
+        assert np.array_equal(r["neg2"], seq["neg2"]) and np.array_equal(r["jitter"], seq["jitter"])
