@@ -509,3 +509,19 @@ def test_concurrent_contexts_in_threads(g):
     assert not errs, errs
     for r in out:
         assert np.array_equal(r["neg2"], seq["neg2"]) and np.array_equal(r["jitter"], seq["jitter"])
+
+
+@pytest.mark.parametrize("precision,tol", [("double", 1e-13), ("single", 1e-5)])
+def test_profile_known_answer_n2(g, ctx, precision, tol):
+    """SPEC.md:245: X = [[0],[1]], y = [0, 1], theta = 2, p = 1.95 -> -2logL = -1.113952892208059,
+    mu = 0.5, sigma2 = 0.28912941068741643, jitter 0; the model predicts 0.5 at x = 0.5."""
+    data = g.new_dataset([[0.0], [1.0]], [0.0, 1.0])
+    ev = g.ProfileEvaluator(data, 1.95, 0.0, g.Backend(ctx), max_batch=1, precision=precision)
+    r = ev.eval(np.array([2.0]))
+    assert rel(r.neg2_log_lik, -1.113952892208059) < tol
+    assert rel(r.mu_hat, 0.5) < tol and rel(r.sigma2_hat, 0.28912941068741643) < tol
+    assert r.jitter_used == 0.0
+    m = g.model_at_theta(data, [2.0], 1.95, 0.0, g.Backend(ctx), precision=precision)
+    assert abs(g.predict(m, [[0.5]])[0] - 0.5) < tol
+    ev.close()
+    m.close()
