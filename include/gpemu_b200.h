@@ -109,6 +109,13 @@ GPEMU_API int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double
                                    size_t d, double p, double nugget, size_t max_batch,
                                    int precision, gpemu_plan** out);
 GPEMU_API int gpemu_plan_precision(const gpemu_plan* plan);
+
+/* Device memory: free / total bytes on the context's device (cudaMemGetInfo), and the bytes a
+ * plan of (n, d, max_batch, precision) allocates (table + max_batch + 1 slots + flags), so a
+ * caller can size max_batch to HBM. gpemu_fit evaluates a population larger than max_batch
+ * in chunks (same candidates, same theta-hat). */
+GPEMU_API int gpemu_ctx_mem_info(gpemu_ctx* ctx, size_t* free_bytes, size_t* total_bytes);
+GPEMU_API size_t gpemu_plan_bytes(size_t n, size_t d, size_t max_batch, int precision);
 GPEMU_API int gpemu_plan_destroy(gpemu_plan* plan);
 GPEMU_API size_t gpemu_plan_device_bytes(const gpemu_plan* plan);
 
@@ -154,7 +161,7 @@ typedef struct {
 } gpemu_fit_result;
 
 /* fit_gp_detailed (likelihood.hpp:243-303): GA over log10(theta) in [lo, hi]
- * with one device batch per generation; the stash keeps the earliest best
+ * with one device batch per generation (chunks of max_batch if the population is larger); the stash keeps the earliest best
  * (generation, slot) exactly like the sequential reference. theta_hat (d),
  * alpha (n), trace_best (generations), trace_genes (generations*d) may be NULL.
  * model_out (nullable) receives a device-resident GpModel for gpemu_predict. */

@@ -457,6 +457,26 @@ int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine) {
 
 uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int gpemu_ctx_mem_info(gpemu_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx) return set_error(GPEMU_VALIDATION, "null ctx");
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  size_t f = 0, tot = 0;
+  ck(cudaMemGetInfo(&f, &tot), "cudaMemGetInfo");
+  if (free_bytes) *free_bytes = f;
+  if (total_bytes) *total_bytes = tot;
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+size_t gpemu_plan_bytes(size_t n, size_t d, size_t max_batch, int precision) {
+  const size_t NT = (n + TILE - 1) / TILE, tiles = NT * (NT + 1) / 2;
+  const size_t elem = precision == GPEMU_PRECISION_SINGLE ? sizeof(float) : sizeof(double);
+  const size_t slots = max_batch + 1;
+  return tiles * TILE_ELEMS * (d * sizeof(double) + slots * elem) + slots * 2 * NT * TILE * elem +
+         slots * (NT + 1) * NT * sizeof(int) + (n * d + n) * sizeof(double);
+}
+
 // ---------------------------------------------------------------------------
 int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
                      double p, double nugget, double* R_out) {
@@ -1058,53 +1078,74 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
   int rc = ga_setup(&ga, pl->d, lo, hi, gac, seed);
   if (rc) return rc;
   const int d = pl->d, P = ga.P;
-  if ((size_t)P > pl->max_batch)
-    return set_error(GPEMU_CONFIG, "fit: population %d exceeds the plan's max_batch %zu", P, pl->max_batch);
-  const int stash = (int)pl->max_batch;  // device slot holding the best factor
+  // A generation larger than the plan's slots is evaluated in chunks of max_batch (batch
+  // invariance: a theta's record does not depend on its slot or batch); the stash is kept
+  // chunk by chunk with the reference's rule (strict < in slot order, likelihood.hpp:267), so
+  // the winning factor is saved before a later chunk reuses its slot.
+  const int MB = (int)pl->max_batch;
+  const int stash = MB;  // device slot holding the best factor
   cudaStream_t s = pl->ctx->stream;
   std::vector<double> thetas((size_t)P * d), fitness(P), stash_theta(d), stash_rec(REC_SIZE, 0.0);
   double jitter_max = 0.0;
+  auto keep_factor = [&](int slot) {
+    if (pl->precision == GPEMU_PRECISION_SINGLE) {
+      ck(cudaMemcpyAsync(pl->factors_f.p + (size_t)stash * pl->slot_stride,
+                         pl->factors_f.p + (size_t)slot * pl->slot_stride,
+                         pl->slot_stride * sizeof(float), cudaMemcpyDeviceToDevice, s),
+         "stash factor");
+      ck(cudaMemcpyAsync(pl->borders_f.p + (size_t)stash * 2 * pl->Npad,
+                         pl->borders_f.p + (size_t)slot * 2 * pl->Npad, 2 * pl->Npad * sizeof(float),
+                         cudaMemcpyDeviceToDevice, s),
+         "stash border");
+    } else {
+      ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
+                         pl->factors.p + (size_t)slot * pl->slot_stride,
+                         pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
+         "stash factor");
+      ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
+                         pl->borders.p + (size_t)slot * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
+                         cudaMemcpyDeviceToDevice, s),
+         "stash border");
+    }
+  };
   while (ga.gen < ga.G) {
-    // objective lambda (likelihood.hpp:264-273) over the whole generation: one batch
+    // objective lambda (likelihood.hpp:264-273) over the generation: one batch per chunk
     ga.thetas(thetas.data());
-    ck(cudaMemcpyAsync(pl->theta.p, thetas.data(), thetas.size() * sizeof(double),
-                       cudaMemcpyHostToDevice, s),
-       "H2D theta");
-    rc = run_batch(pl, P);
-    if (rc) return rc;
-    download_records(pl, P);
     const double prev_stash = ga.stash_value;
-    for (int i = 0; i < P; ++i) {
-      fitness[i] = pl->h_out[(size_t)i * REC_SIZE + REC_NEG2];
-      if (pl->last_ladder[i] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[i]]);
+    double best = prev_stash;
+    int best_i = -1;
+    for (int c0 = 0; c0 < P; c0 += MB) {
+      const int cn = std::min(MB, P - c0);
+      ck(cudaMemcpyAsync(pl->theta.p, thetas.data() + (size_t)c0 * d, (size_t)cn * d * sizeof(double),
+                         cudaMemcpyHostToDevice, s),
+         "H2D theta");
+      rc = run_batch(pl, cn);
+      if (rc) return rc;
+      download_records(pl, cn);
+      int chunk_best = -1;
+      for (int q = 0; q < cn; ++q) {
+        const int i = c0 + q;
+        const double* r = &pl->h_out[(size_t)q * REC_SIZE];
+        fitness[i] = r[REC_NEG2];
+        if (pl->last_ladder[q] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[q]]);
+        if (fitness[i] < best) {  // strict <: the earliest slot wins ties
+          best = fitness[i];
+          best_i = i;
+          chunk_best = q;
+        }
+      }
+      if (chunk_best >= 0) {  // keep this chunk's winner before the next chunk reuses the slot
+        const double* r = &pl->h_out[(size_t)chunk_best * REC_SIZE];
+        std::copy(r, r + REC_SIZE, stash_rec.begin());
+        std::copy(&thetas[(size_t)best_i * d], &thetas[(size_t)best_i * d] + d, stash_theta.begin());
+        keep_factor(chunk_best);
+      }
     }
     const int gen_now = ga.gen;
     ga.tell(fitness.data());
-    if (ga.stash_value < prev_stash && ga.stash_gen == gen_now) {
-      const int i = ga.stash_slot;  // keep the best factor on the device (likelihood.hpp:270)
-      const double* r = &pl->h_out[(size_t)i * REC_SIZE];
-      std::copy(r, r + REC_SIZE, stash_rec.begin());
-      std::copy(&thetas[(size_t)i * d], &thetas[(size_t)i * d] + d, stash_theta.begin());
-      if (pl->precision == GPEMU_PRECISION_SINGLE) {
-        ck(cudaMemcpyAsync(pl->factors_f.p + (size_t)stash * pl->slot_stride,
-                           pl->factors_f.p + (size_t)i * pl->slot_stride,
-                           pl->slot_stride * sizeof(float), cudaMemcpyDeviceToDevice, s),
-           "stash factor");
-        ck(cudaMemcpyAsync(pl->borders_f.p + (size_t)stash * 2 * pl->Npad,
-                           pl->borders_f.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(float),
-                           cudaMemcpyDeviceToDevice, s),
-           "stash border");
-      } else {
-        ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
-                           pl->factors.p + (size_t)i * pl->slot_stride,
-                           pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
-           "stash factor");
-        ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
-                           pl->borders.p + (size_t)i * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
-                           cudaMemcpyDeviceToDevice, s),
-           "stash border");
-      }
-    }
+    const bool improved = ga.stash_value < prev_stash && ga.stash_gen == gen_now;
+    if (improved != (best_i >= 0) || (improved && ga.stash_slot != best_i))
+      return set_error(GPEMU_ERROR, "fit: evaluation stash diverged from the optimizer's");
   }
   ck(cudaStreamSynchronize(s), "fit");
   if (!std::isfinite(ga.stash_value))

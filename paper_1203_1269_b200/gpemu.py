@@ -76,6 +76,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
     "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
+    "gpemu_ctx_mem_info", "gpemu_plan_bytes",
 )
 
 
@@ -142,6 +143,9 @@ def lib():
     L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_scalars.argtypes = [_vp, _dp]
+    L.gpemu_ctx_mem_info.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
+    L.gpemu_plan_bytes.argtypes = [_sz, _sz, _sz, C.c_int]
+    L.gpemu_plan_bytes.restype = _sz
     L.gpemu_refine_fit_ex.argtypes = [_vp, _vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                       C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_destroy.argtypes = [_vp]
@@ -766,6 +770,28 @@ class GeneticOptimizer:
             pass
 
 
+def fit_batch(data: Dataset, cfg: FitConfig, backend: Backend, reserve: float = 0.9) -> int:
+    """Candidate slots for a fit: the whole GA population when its plan fits in `reserve` of the
+    free device memory, else as many as fit (the generation is then evaluated in chunks, with
+    the same candidates and the same theta-hat)."""
+    prec = PRECISIONS[parse_precision(cfg.precision)]
+    P = cfg.ga.population
+    free, tot = C.c_size_t(), C.c_size_t()
+    _check(lib().gpemu_ctx_mem_info(backend.ctx.handle, C.byref(free), C.byref(tot)))
+    budget = reserve * free.value
+    n, d = data.n(), data.d()
+    if lib().gpemu_plan_bytes(n, d, P, prec) <= budget:
+        return P
+    lo, hi = 1, P
+    while lo < hi:  # largest max_batch whose plan fits
+        mid = (lo + hi + 1) // 2
+        if lib().gpemu_plan_bytes(n, d, mid, prec) <= budget:
+            lo = mid
+        else:
+            hi = mid - 1
+    return lo
+
+
 def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
                     evaluator: Optional[ProfileEvaluator] = None) -> FitResult:
     """likelihood.hpp:243-303: one device batch per GA generation."""
@@ -773,7 +799,8 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
     bounds = cfg.bounds_for(d)
     own = evaluator is None
     ev = evaluator or ProfileEvaluator(data, cfg.p, cfg.nugget, backend,
-                                       max_batch=cfg.ga.population, precision=cfg.precision)
+                                       max_batch=fit_batch(data, cfg, backend),
+                                       precision=cfg.precision)
     try:
         lo = _f64([b[0] for b in bounds])
         hi = _f64([b[1] for b in bounds])

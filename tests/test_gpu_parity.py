@@ -525,3 +525,22 @@ def test_profile_known_answer_n2(g, ctx, precision, tol):
     assert abs(g.predict(m, [[0.5]])[0] - 0.5) < tol
     ev.close()
     m.close()
+
+
+def test_fit_population_in_chunks(g, ctx):
+    """A plan with fewer slots than the GA population evaluates each generation in chunks: the same
+    candidates, the same stash (strict < in slot order) -- theta-hat, trace and model identical to
+    the one-batch fit. fit_batch sizes the plan to device memory (whole population when it fits)."""
+    z = np.load(os.path.join(GOLD, "c1p195.npz"))
+    data = g.new_dataset(z["X"], z["y"])
+    be = g.Backend(ctx)
+    cfg = g.FitConfig(ga=g.GaConfig(population=20, generations=4), seed=3, p=1.95)
+    assert g.fit_batch(data, cfg, be) == 20
+    full = g.fit_gp_detailed(data, cfg, be)
+    ev7 = g.ProfileEvaluator(data, 1.95, 0.0, be, max_batch=7)
+    part = g.fit_gp_detailed(data, cfg, be, evaluator=ev7)
+    assert np.array_equal(np.array(part.model.params.theta), np.array(full.model.params.theta))
+    assert part.model.neg2_log_lik == full.model.neg2_log_lik
+    assert [r.best_value for r in part.trace.generations] == [r.best_value for r in full.trace.generations]
+    assert np.array_equal(part.model.alpha, full.model.alpha)
+    ev7.close()
