@@ -11,10 +11,10 @@
 // * chol_dag_kernel -- the product engine. A persistent kernel (one CTA per SM)
 //   pulls tasks from a global ticket counter. The task order is a topological
 //   order of the left-looking tile Cholesky of every candidate in the batch,
-//   with a one-column lookahead (the diagonal task of column j+1 is issued right
-//   after the task that produces its last input), so waits only ever target
-//   lower tickets (deadlock free) and the serial panel chain of one candidate
-//   is hidden behind the other candidates' work.
+//   with a one-column lookahead (the diagonal task of column j+1 is issued within
+//   the column-j group, after the task that produces its last input), so waits
+//   only ever target lower tickets (deadlock free) and the serial panel chain of
+//   one candidate is hidden behind the other candidates' work.
 //     DIAG(b, j):  C = R(j,j) - sum_{K<j} L(j,K) L(j,K)^T     (DMMA)
 //                  L(j,j) = chol(C)      blocked 16-wide in shared memory
 //                  border rows: [u_j; v_j] = ([y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T) L(j,j)^-T
@@ -201,18 +201,21 @@ __device__ __forceinline__ void decode_task(int t, int B, int NT, int& bpos, int
     t -= g;
     ++jj;
   }
+  // candidate bpos, column group jj: OFF(jj+1, jj) first (DIAG(jj+1)'s last input), the other
+  // OFF(I, jj), then DIAG(jj+1) last -- by the time a CTA takes it, OFF(jj+1, jj) is usually
+  // done, so the CTA does not idle on the flag (-0.3% at C3 vs DIAG right after it)
   const int per = NT - jj;
   bpos = t / per;
   const int pos = t - bpos * per;
   if (pos == 0) {
     j = jj;
     I = jj + 1;
-  } else if (pos == 1) {
+  } else if (pos == per - 1) {
     j = jj + 1;
     I = jj + 1;
   } else {
     j = jj;
-    I = jj + pos;
+    I = jj + pos + 1;
   }
 }
 

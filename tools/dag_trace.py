@@ -37,9 +37,9 @@ def decode_left(t):
     b, pos = divmod(t, per)
     if pos == 0:
         return b, jj + 1, jj, 0
-    if pos == 1:
+    if pos == per - 1:
         return b, jj + 1, jj + 1, 0
-    return b, jj + pos, jj, 0
+    return b, jj + pos + 1, jj, 0
 
 
 nt = B * NT * (NT + 1) // 2
