@@ -544,3 +544,20 @@ def test_fit_population_in_chunks(g, ctx):
     assert [r.best_value for r in part.trace.generations] == [r.best_value for r in full.trace.generations]
     assert np.array_equal(part.model.alpha, full.model.alpha)
     ev7.close()
+
+
+def test_single_precision_deep_ladder(g, ctx, ref_fast):
+    """A near-rank-1 R (theta -> 0, n=3000) fails the float factorization until jitter 1e-5 in
+    the reference's float instantiation (backend.hpp:105-119); the device float engine climbs
+    the ladder to the same step and agrees within the float path's error."""
+    rng = np.random.default_rng(31)
+    X = rng.random((3000, 2))
+    y = np.sin(3 * X).sum(1)
+    th = np.array([[1e-6, 1e-6], [1.0, 2.0]])
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=2,
+                            precision="single")
+    r = ev.eval_batch(th)
+    fs = ref_fast.eval_batch(X, y, th, 1.95, threads=0, precision="single")
+    assert np.array_equal(r["jitter"], fs["jitter"]) and r["jitter"][0] == 1e-5
+    assert np.all(np.abs(r["neg2"] - fs["neg2"]) <= 1e-3 * np.abs(fs["neg2"]))
+    ev.close()
