@@ -110,7 +110,9 @@ GPEMU_API int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double
                                    int precision, gpemu_plan** out);
 GPEMU_API int gpemu_plan_precision(const gpemu_plan* plan);
 
-/* Device memory: free / total bytes on the context's device (cudaMemGetInfo), and the bytes a
+/* Device memory: free / total bytes on the context's device (cudaMemGetInfo, plus the pages
+ * the engine's memory pool keeps mapped for the next plan: plans and models allocate from a
+ * per-device stream-ordered pool that is trimmed when a context is destroyed), and the bytes a
  * plan of (n, d, max_batch, precision) allocates (table + max_batch + 1 slots + flags), so a
  * caller can size max_batch to HBM. gpemu_fit evaluates a population larger than max_batch
  * in chunks (same candidates, same theta-hat). */

@@ -19,7 +19,9 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdint>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <random>
 #include <string>
@@ -55,21 +57,92 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr double kLadder[6] = {0.0, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4};  // backend.hpp:77
 
+// Device memory: one stream-ordered pool per device, owned by the library, that keeps freed
+// blocks mapped (release threshold = max). A plan holds gigabytes (C3: 6.9 GB of factors and
+// table); cudaMalloc / cudaFree of those per plan cost 1-700 ms each on the box, more than the
+// GA fit itself at the paper's sizes, and the paper protocol builds a plan per replication.
+// With the pool a new plan reuses the previous plan's pages. The pool is trimmed when an
+// allocation would not fit otherwise and when a context is destroyed.
+struct DevPool {
+  cudaMemPool_t pool = nullptr;
+  cudaStream_t stream = nullptr;  // allocation stream, synchronised after every allocation
+};
+
+DevPool& dev_pool(int dev) {
+  static std::mutex mu;
+  static DevPool pools[64];
+  if (dev < 0 || dev >= 64) throw CudaError{"device index out of range"};
+  std::lock_guard<std::mutex> lock(mu);
+  DevPool& P = pools[dev];
+  if (!P.pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    ck(cudaMemPoolCreate(&P.pool, &props), "cudaMemPoolCreate");
+    uint64_t keep = UINT64_MAX;
+    ck(cudaMemPoolSetAttribute(P.pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+    int cur = 0;
+    ck(cudaGetDevice(&cur), "cudaGetDevice");
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&P.stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaSetDevice(cur), "cudaSetDevice");
+  }
+  return P;
+}
+
+// Bytes the pool holds mapped but not handed out (free for the next plan).
+size_t pool_idle_bytes(int dev) {
+  DevPool& P = dev_pool(dev);
+  uint64_t reserved = 0, used = 0;
+  ck(cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrReservedMemCurrent, &reserved), "cudaMemPoolGetAttribute");
+  ck(cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrUsedMemCurrent, &used), "cudaMemPoolGetAttribute");
+  return reserved > used ? static_cast<size_t>(reserved - used) : 0;
+}
+
+void pool_trim(int dev) {
+  DevPool& P = dev_pool(dev);
+  ck(cudaStreamSynchronize(P.stream), "cudaStreamSynchronize");
+  ck(cudaMemPoolTrimTo(P.pool, 0), "cudaMemPoolTrimTo");
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
+  int dev = -1;
   void alloc(size_t c) {
     free();
     if (c == 0) c = 1;
-    ck(cudaMalloc(&p, c * sizeof(T)), "cudaMalloc");
+    ck(cudaGetDevice(&dev), "cudaGetDevice");
+    DevPool& P = dev_pool(dev);
+    void* q = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&q, c * sizeof(T), P.pool, P.stream);
+    if (e == cudaErrorMemoryAllocation) {  // idle pool pages are not enough: release them, retry
+      (void)cudaGetLastError();
+      ck(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+      ck(cudaMemPoolTrimTo(P.pool, 0), "cudaMemPoolTrimTo");
+      e = cudaMallocFromPoolAsync(&q, c * sizeof(T), P.pool, P.stream);
+    }
+    ck(e, "cudaMallocFromPoolAsync");
+    ck(cudaStreamSynchronize(P.stream), "cudaStreamSynchronize");  // usable from any stream
+    p = static_cast<T*>(q);
     count = c;
   }
   void reserve(size_t c) {  // grow-only: keeps the allocation when it is large enough
     if (count < c) alloc(c);
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p) {
+      // cudaFree's implicit device synchronisation, kept: no kernel may still use the block
+      // when the pool hands it to the next allocation
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (cur != dev) cudaSetDevice(dev);
+      cudaDeviceSynchronize();
+      cudaFreeAsync(p, dev_pool(dev).stream);
+      if (cur != dev && cur >= 0) cudaSetDevice(cur);
+    }
     p = nullptr;
     count = 0;
   }
@@ -437,7 +510,12 @@ int gpemu_ctx_destroy(gpemu_ctx* ctx) {
   if (!ctx) return GPEMU_OK;
   delete ctx->scratch;
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  const int dev = ctx->device;
   delete ctx;
+  try {  // hand the idle pool pages back to the driver (other CUDA users in the process)
+    pool_trim(dev);
+  } catch (const CudaError&) {
+  }
   return GPEMU_OK;
 }
 
@@ -463,6 +541,7 @@ int gpemu_ctx_mem_info(gpemu_ctx* ctx, size_t* free_bytes, size_t* total_bytes) 
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   size_t f = 0, tot = 0;
   ck(cudaMemGetInfo(&f, &tot), "cudaMemGetInfo");
+  f += pool_idle_bytes(ctx->device);  // mapped by the engine's pool but free for the next plan
   if (free_bytes) *free_bytes = f;
   if (total_bytes) *total_bytes = tot;
   return GPEMU_OK;
