@@ -746,17 +746,37 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           publish_flag(&flags[j * NT + j], epoch);
           pr.lap(PR_DIAG_STORE);
         }
-        // border solve: [u_j; v_j] = w L(j,j)^-T (column-oriented substitution)
-        if (ok && warp < 2) {
-          double* w = W + warp * TILE;
-          for (int c = 0; c < TILE; ++c) {
-            const double x = div_by(w[c], Cs(C, c, c), rinvD[c]);
-            __syncwarp();
-            for (int l = c + 1 + lane; l < TILE; l += 32) w[l] -= x * Cs(C, l, c);
-            if (lane == 0) w[c] = x;
-            __syncwarp();
+        // border solve: [u_j; v_j] = w L(j,j)^-T, blocked by 16 columns: lanes 0/1 of warp 0
+        // substitute the block in registers, then every consumer thread updates one (row,
+        // column) right of it with the block's 16 products. Each w element receives the same
+        // FMAs in the same column order as a column-by-column substitution.
+        if (ok) {
+          double* Dd = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);  // [8][16][16], idle ring tail
+          for (int q = tid; q < 2048; q += kConsumers) {
+            const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
+            Dd[q] = cc <= rr ? Cs(C, 16 * b8 + rr, 16 * b8 + cc) : 0.0;
           }
-          for (int l = lane; l < TILE; l += 32) __stcg(bord + warp * Npad + j * TILE + l, w[l]);
+          consumer_sync();
+          for (int cb = 0; cb < 8; ++cb) {
+            const int o = 16 * cb;
+            if (warp == 0 && lane < 2) {
+              double xr[16];
+              load_row16(xr, W + lane * TILE + o);
+              solve_row16(xr, Dd + cb * 256, rinvD + o);
+              store_row16(xr, W + lane * TILE + o);
+            }
+            consumer_sync();
+            const int l = o + 16 + bc;
+            if (l < TILE) {
+              const double* x = W + brow * TILE + o;
+              double s = W[brow * TILE + l];
+#pragma unroll
+              for (int c = 0; c < 16; ++c) s -= x[c] * Cs(C, l, o + c);
+              W[brow * TILE + l] = s;
+            }
+            consumer_sync();
+          }
+          if (tid < 2 * TILE) __stcg(bord + brow * Npad + j * TILE + bc, W[brow * TILE + bc]);
         }
         consumer_sync();
         if (tid == 0) {
