@@ -630,11 +630,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
         const int stage = itp % kStages;
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
-        mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes : kStageBytes);
+        mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes + 2 * SLAB * 8 : kStageBytes);
         bulk_g2s(dst, a_tile(K) + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
-        if (!diag)
+        if (!diag) {
           bulk_g2s(dst + kSlabBytes, fac + tile_index(j, K) * TILE_ELEMS + sq * SLAB_ELEMS,
                    kSlabBytes, &full[stage]);
+        } else {  // the slab's border segments [u_K; v_K] ride in the unused B half
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+            bulk_g2s(dst + kSlabBytes + r * SLAB * 8, bord + r * Npad + K * TILE + sq * SLAB, SLAB * 8,
+                     &full[stage]);
+        }
       };
       // Prologue: the first kStages slabs. Afterwards the LAST warp to finish with a
       // stage refills it (slab q + kStages): no warp ever blocks waiting for the others.
@@ -687,11 +693,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           }
         }
         if (diag) {
-          // border rows: wacc -= sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk]
-          const int K = q >> 2, sq = q & 3;
-          const double* ub = bord + brow * Npad + K * TILE + sq * SLAB;
+          // border rows: wacc -= sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk], the u_K
+          // segment from the stage (broadcast loads)
+          const double* ub = As + SLAB_ELEMS + brow * SLAB;
 #pragma unroll 8
-          for (int kk = 0; kk < SLAB; ++kk) wacc -= __ldcg(ub + kk) * Bs[slab_off(bc, kk)];
+          for (int kk = 0; kk < SLAB; ++kk) wacc -= ub[kk] * Bs[slab_off(bc, kk)];
         }
         __syncwarp();
         if (lane == 0) {
