@@ -593,17 +593,32 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // (the upper triangle is skipped, balanced across warps).
       const int rowA = diag ? 8 * warp + lr : 16 * warp + lr;
       const int rowB = diag ? 8 * (15 - warp) + lr : 16 * warp + 8 + lr;
+      // DIAG tasks use 17 accumulator slots s = 16 mi + ni, fixed at compile time: slot
+      // s <= warp is (m-tile w, n-tile s), slot s > warp is (m-tile 15 - w, n-tile s - w - 1), so
+      // the lower-triangle mainloop issues exactly 17 unpredicated DMMAs per k-step.
       double acc[2][16][2];
+      if (!diag) {
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+        for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 16; ++ni) {
-          const int off = acc_off(mi ? rowB : rowA, ni, lc);
-          const double2 v = skip ? make_double2(0.0, 0.0)
-                                 : __ldcg(reinterpret_cast<const double2*>(gtile + off));
-          acc[mi][ni][0] = v.x;
-          acc[mi][ni][1] = v.y;
+          for (int ni = 0; ni < 16; ++ni) {
+            const double2 v = skip ? make_double2(0.0, 0.0)
+                                   : __ldcg(reinterpret_cast<const double2*>(gtile + acc_off(mi ? rowB : rowA, ni, lc)));
+            acc[mi][ni][0] = v.x;
+            acc[mi][ni][1] = v.y;
+          }
+      } else {
+#pragma unroll
+        for (int sl = 0; sl < 32; ++sl) {
+          const bool first = sl <= warp;
+          const double2 v = (skip || sl >= 17)
+                                ? make_double2(0.0, 0.0)
+                                : __ldcg(reinterpret_cast<const double2*>(
+                                      gtile + acc_off(first ? rowA : rowB, first ? sl : sl - warp - 1, lc)));
+          acc[sl >> 4][sl & 15][0] = v.x;
+          acc[sl >> 4][sl & 15][1] = v.y;
         }
+      }
       // border rows (DIAG): running residual of [y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T
       double wacc = (diag && !skip) ? __ldcg(bord + brow * Npad + j * TILE + bc) : 0.0;
 
@@ -682,13 +697,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           for (int ks = 0; ks < 8; ++ks) {
             const int ko = (ks ^ lr) << 2;
             const double a0 = -Aw0[ko], a1 = -Aw1[ko];
+            const double* BwB = Bw - (warp + 1) * 256;  // slot sl > warp reads n-tile sl - warp - 1
 #pragma unroll
-            for (int ni = 0; ni < 16; ++ni) {
-              if (ni <= warp || ni <= 15 - warp) {
-                const double b = Bw[ni * 256 + ko];
-                if (ni <= warp) dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
-                if (ni <= 15 - warp) dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
-              }
+            for (int sl = 0; sl < 17; ++sl) {
+              const bool first = sl <= warp;
+              const double b = (first ? Bw : BwB)[sl * 256 + ko];
+              dmma884(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1], first ? a0 : a1, b);
             }
           }
         }
@@ -725,12 +739,13 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // ------------------------------ DIAG ------------------------------
         // accumulators (= R - sum L L^T) -> C (tile layout); the POTRF runs in its own
         // (non-inlined) function so its register pressure stays out of the mainloop
+        // (the upper triangle of C is left as is: nothing downstream reads it)
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 16; ++ni)
-            *reinterpret_cast<double2*>(C + acc_off(mi ? rowB : rowA, ni, lc)) =
-                make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+        for (int sl = 0; sl < 17; ++sl) {
+          const bool first = sl <= warp;
+          *reinterpret_cast<double2*>(C + acc_off(first ? rowA : rowB, first ? sl : sl - warp - 1, lc)) =
+              make_double2(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1]);
+        }
         consumer_sync();
         if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
