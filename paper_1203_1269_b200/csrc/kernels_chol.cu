@@ -346,47 +346,46 @@ __device__ __forceinline__ int p_off(int r, int c) {
 }
 
 // Pivot root and reciprocal without the sqrt / DDIV call sequences: y ~ 1/sqrt(s) from
-// rsqrt.approx + two Newton steps (~1 ulp), d = s*y corrected once (Markstein: the correctly
-// rounded sqrt except in rare ties), r = y as the approximate reciprocal that div_by corrects
-// with one FMA residual. Evaluated redundantly by every lane from the broadcast pivot.
+// rsqrt.approx.f64, which sm_100a implements as MUFU.RSQ64H plus one refinement (max relative
+// error 2^-53 measured, tools/probes/rsqrt_acc.cu), d = s*y corrected once (Markstein: the
+// correctly rounded sqrt except in rare ties), r = y as the approximate reciprocal that
+// div_by corrects with one FMA residual. Evaluated redundantly by every lane from the
+// broadcast pivot.
 __device__ __forceinline__ void pivot_root(double s, double& d, double& r) {
   double y;
   asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(s));
-  const double hs = 0.5 * s;
-  y = fma(y, fma(-hs * y, y, 0.5), y);
-  y = fma(y, fma(-hs * y, y, 0.5), y);
   const double d0 = s * y;
   d = fma(fma(-d0, d0, s), 0.5 * y, d0);
   r = y;
 }
 
 // In-register Cholesky of a 16x16 diagonal block, lane r (< 16) holding row r in xr.
-// Right-looking: column c is broadcast through colbuf. Pivot reciprocals -> rinv[0..15].
-// Returns false (uniform) on a failed pivot (backend.hpp:238).
-__device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* colbuf, double* rinv, int lane) {
-  bool ok = true;  // uniform: every lane sees the same pivots (no divergent exit in the loop)
+// Right-looking, branch-free and register-only: the quotients of column c are broadcast by
+// shuffles, and the next pivot (lane c+1's diagonal minus its own quotient squared) is
+// formed and rooted before column c's updates are applied, so the serial pivot chain is
+// shfl -> root -> div -> fma with the updates filling its latency. Every lower-triangle
+// element gets the same operations in the same order as a column-by-column right-looking
+// loop; the upper triangle of xr is left undefined (never read). Pivot reciprocals ->
+// rinv[0..15]. Returns false (uniform) on a failed pivot (backend.hpp:238).
+__device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int lane) {
+  double d, r;
+  double s = __shfl_sync(0xffffffffu, xr[0], 0);
+  bool ok = s > 0.0;  // uniform: every lane sees the same pivots
+  if (!ok) s = 1.0;   // keep the arithmetic finite after a failure; the block is discarded
+  pivot_root(s, d, r);
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
-    double s = __shfl_sync(0xffffffffu, xr[c], c);
-    ok = ok && s > 0.0;
-    if (!ok) s = 1.0;  // keep the arithmetic finite after a failure; the block is discarded
-    double d, r;
-    pivot_root(s, d, r);
-    if (lane == c) {
-      xr[c] = d;
-      rinv[c] = r;
+    const double q = div_by(xr[c], d, r);
+    if (lane == c) rinv[c] = r;
+    xr[c] = lane > c ? q : (lane == c ? d : xr[c]);
+    if (c < 15) {  // the next pivot first: it depends only on lane c+1's own quotient
+      double sn = __shfl_sync(0xffffffffu, fma(-q, q, xr[c + 1]), c + 1);
+      ok = ok && sn > 0.0;
+      if (!ok) sn = 1.0;
+      pivot_root(sn, d, r);
     }
-    if (lane > c && lane < 16) {
-      xr[c] = div_by(xr[c], d, r);
-      colbuf[lane] = xr[c];
-    }
-    __syncwarp();
-    if (lane > c && lane < 16) {
 #pragma unroll
-      for (int c2 = c + 1; c2 < 16; ++c2)
-        if (c2 <= lane) xr[c2] -= xr[c] * colbuf[c2];
-    }
-    __syncwarp();
+    for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] = fma(-q, __shfl_sync(0xffffffffu, q, c2), xr[c2]);
   }
   return ok;
 }
@@ -419,15 +418,27 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   double* Dblk = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [16][16]
   double* P = Dblk + 256;                                                     // [128][16]
   double* Stw = P + TILE * 16 + warp * (16 * kStageLd);                       // per warp
-  double* colbuf = P + TILE * 16 + kConsumerWarps * 16 * kStageLd;            // [16]
+#ifdef GPEMU_POTRF_PROF
+  long long tp[8][4];
+  const long long tstart = clock64();
+#endif
   for (int kb = 0; kb < 8; ++kb) {
     const int o = 16 * kb;
+#ifdef GPEMU_POTRF_PROF
+    tp[kb][0] = clock64();
+#endif
     if (warp == kb) {
       stage_out(acc, Stw, lr, lc);
       __syncwarp();
       double xr[16];
       if (lane < 16) load_row16(xr, Stw + lane * kStageLd);
-      const bool okw = potrf_row16(xr, colbuf, rinvD + o, lane);
+#ifdef GPEMU_POTRF_PROF
+      const long long tq = clock64();
+#endif
+      const bool okw = potrf_row16(xr, rinvD + o, lane);
+#ifdef GPEMU_POTRF_PROF
+      if (lane == 0) misc->pad = (int)(clock64() - tq);
+#endif
       if (!okw && lane == 0) misc->fail = 1;
       if (lane < 16) {
         store_row16(xr, Stw + lane * kStageLd);
@@ -437,6 +448,10 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       stage_in(acc, Stw, lr, lc);
     }
     consumer_sync();
+#ifdef GPEMU_POTRF_PROF
+    tp[kb][1] = clock64();
+    tp[kb][3] = misc->pad;
+#endif
     if (misc->fail) return false;
     if (warp > kb) {
       stage_out(acc, Stw, lr, lc);
@@ -463,6 +478,9 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
               make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
     }
     consumer_sync();  // the panel buffer is complete
+#ifdef GPEMU_POTRF_PROF
+    tp[kb][2] = clock64();
+#endif
     if (warp > kb) {
       double av[2][4];
       window_afrags(acc, av, lane);
@@ -482,6 +500,16 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       rotate_window(acc);
     }
   }
+#ifdef GPEMU_POTRF_PROF
+  if (threadIdx.x == 0 && (misc->j == 6 || misc->j == 20)) {
+    const long long tend = clock64();
+    for (int kb = 0; kb < 8; ++kb)
+      printf("POTRF j %d kb %d: step %lld potrf16 %lld (in-warp %lld) panel %lld rest %lld\n", misc->j, kb,
+             (kb < 7 ? tp[kb + 1][0] : tend) - tp[kb][0], tp[kb][1] - tp[kb][0], tp[kb][3],
+             tp[kb][2] - tp[kb][1], (kb < 7 ? tp[kb + 1][0] : tend) - tp[kb][2]);
+    printf("POTRF j %d total %lld\n", misc->j, tend - tstart);
+  }
+#endif
   return true;
 }
 
