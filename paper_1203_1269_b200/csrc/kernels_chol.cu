@@ -418,27 +418,14 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   double* Dblk = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [16][16]
   double* P = Dblk + 256;                                                     // [128][16]
   double* Stw = P + TILE * 16 + warp * (16 * kStageLd);                       // per warp
-#ifdef GPEMU_POTRF_PROF
-  long long tp[8][4];
-  const long long tstart = clock64();
-#endif
   for (int kb = 0; kb < 8; ++kb) {
     const int o = 16 * kb;
-#ifdef GPEMU_POTRF_PROF
-    tp[kb][0] = clock64();
-#endif
     if (warp == kb) {
       stage_out(acc, Stw, lr, lc);
       __syncwarp();
       double xr[16];
       if (lane < 16) load_row16(xr, Stw + lane * kStageLd);
-#ifdef GPEMU_POTRF_PROF
-      const long long tq = clock64();
-#endif
       const bool okw = potrf_row16(xr, rinvD + o, lane);
-#ifdef GPEMU_POTRF_PROF
-      if (lane == 0) misc->pad = (int)(clock64() - tq);
-#endif
       if (!okw && lane == 0) misc->fail = 1;
       if (lane < 16) {
         store_row16(xr, Stw + lane * kStageLd);
@@ -448,10 +435,6 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       stage_in(acc, Stw, lr, lc);
     }
     consumer_sync();
-#ifdef GPEMU_POTRF_PROF
-    tp[kb][1] = clock64();
-    tp[kb][3] = misc->pad;
-#endif
     if (misc->fail) return false;
     if (warp > kb) {
       stage_out(acc, Stw, lr, lc);
@@ -478,9 +461,6 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
               make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
     }
     consumer_sync();  // the panel buffer is complete
-#ifdef GPEMU_POTRF_PROF
-    tp[kb][2] = clock64();
-#endif
     if (warp > kb) {
       double av[2][4];
       window_afrags(acc, av, lane);
@@ -500,16 +480,6 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       rotate_window(acc);
     }
   }
-#ifdef GPEMU_POTRF_PROF
-  if (threadIdx.x == 0 && (misc->j == 6 || misc->j == 20)) {
-    const long long tend = clock64();
-    for (int kb = 0; kb < 8; ++kb)
-      printf("POTRF j %d kb %d: step %lld potrf16 %lld (in-warp %lld) panel %lld rest %lld\n", misc->j, kb,
-             (kb < 7 ? tp[kb + 1][0] : tend) - tp[kb][0], tp[kb][1] - tp[kb][0], tp[kb][3],
-             tp[kb][2] - tp[kb][1], (kb < 7 ? tp[kb + 1][0] : tend) - tp[kb][2]);
-    printf("POTRF j %d total %lld\n", misc->j, tend - tstart);
-  }
-#endif
   return true;
 }
 
