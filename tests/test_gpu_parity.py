@@ -561,3 +561,42 @@ def test_single_precision_deep_ladder(g, ctx, ref_fast):
     assert np.array_equal(r["jitter"], fs["jitter"]) and r["jitter"][0] == 1e-5
     assert np.all(np.abs(r["neg2"] - fs["neg2"]) <= 1e-3 * np.abs(fs["neg2"]))
     ev.close()
+
+
+def test_device_memory_pool(g):
+    """Plans allocate from the library's per-device pool: a destroyed plan's pages stay mapped
+    (reported free by gpemu_ctx_mem_info, reused by the next plan with identical results) and go
+    back to the driver when the context is destroyed."""
+    import ctypes as C
+    import torch
+    torch.cuda.init()
+    mib = 1 << 20
+    n, d, B = 4096, 4, 8
+    plan_bytes = g.lib().gpemu_plan_bytes(n, d, B, 0)
+    assert plan_bytes > 512 * mib
+    rng = np.random.default_rng(5)
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1)
+    th = 10 ** rng.uniform(-1.0, 0.5, size=(B, d))
+    driver0 = torch.cuda.mem_get_info()[0]
+    ctx = g.Context(0)
+
+    def engine_free():
+        f, t = C.c_size_t(), C.c_size_t()
+        g._check(g.lib().gpemu_ctx_mem_info(ctx.handle, C.byref(f), C.byref(t)))
+        return f.value
+
+    f0 = engine_free()
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=B)
+    r1 = ev.eval_batch(th)
+    assert f0 - engine_free() >= 0.9 * plan_bytes
+    ev.close()
+    assert abs(engine_free() - f0) < 64 * mib  # idle pool pages count as free
+    assert torch.cuda.mem_get_info()[0] < driver0 - plan_bytes // 2  # ...and stay mapped
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=B)
+    r2 = ev.eval_batch(th)
+    for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+        assert np.array_equal(r1[k], r2[k]), k
+    ev.close()
+    ctx.close()
+    assert torch.cuda.mem_get_info()[0] > driver0 - 64 * mib  # trimmed on context destroy
