@@ -135,7 +135,7 @@ struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's 
   int bpos;
   int I, j;
   unsigned ljj_phase;  // uses of ljj_bar (the OFF-task L(j,j) load)
-  int pad;
+  int next;           // ticket taken ahead (prefetch of its seed tile), -1: none
   long long t_begin;   // PR_TOTAL start (profiling)
 };
 
@@ -520,12 +520,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   Prof pr{(a.prof && tid == 0) ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr, 0};
   if (tid == 0) {
     misc->ljj_phase = 0;
+    misc->next = -1;
     misc->t_begin = clock64();
   }
+  // Large batches take their next ticket when the mainloop ends and prefetch that task's R
+  // seed tile into L2 while the epilogue runs (the seed is otherwise an HBM read at task
+  // start). Small batches and the last two rounds of tickets do not: a ticket held by a busy
+  // CTA would delay a chain that an idle CTA could start at once.
+  const bool take_ahead = !ext && ntasks >= 16 * (int)gridDim.x;
   pr.start();
   while (true) {
     if (tid == 0) {
-      const int t = atomicAdd(a.counter, 1);
+      const int t = misc->next >= 0 ? misc->next : atomicAdd(a.counter, 1);
+      misc->next = -1;
       misc->ticket = t;
       misc->skip = 0;
       misc->fail = 0;
@@ -727,6 +734,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       }
       consumer_sync();  // every consumer is done reading the stage ring
       stamp(1);
+      if (take_ahead && tid == 0 && misc->ticket < ntasks - 2 * (int)gridDim.x) {
+        const int tn = atomicAdd(a.counter, 1);
+        misc->next = tn;
+        if (tn < ntasks) {
+          int bn = 0, jn, In;
+          decode_task(tn, B, NT, bn, jn, In);
+          const double* seed = a.factors + (size_t)a.slots[bn] * a.slot_stride + tile_index(In, jn) * TILE_ELEMS;
+#pragma unroll
+          for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4) bulk_prefetch_l2(seed + s4 * SLAB_ELEMS, kSlabBytes);
+        }
+      }
       if (tid == 0) {
         pr.lap(PR_GEMM);
         pr.add(PR_SLABS, nslab);
