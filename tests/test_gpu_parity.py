@@ -600,3 +600,22 @@ def test_device_memory_pool(g):
     ev.close()
     ctx.close()
     assert torch.cuda.mem_get_info()[0] > driver0 - 64 * mib  # trimmed on context destroy
+
+
+@pytest.mark.parametrize("n", [127, 128, 129, 255, 256, 257])
+def test_eval_tile_boundaries_vs_reference(g, ctx, ref_fast, n):
+    """Sizes on either side of the 128-row tile (identity padding of the last tile, one vs two
+    tile columns): the same jitter step as the reference's evaluator and deviance / mu / sigma2
+    within rounding of it."""
+    rng = np.random.default_rng(1000 + n)
+    d = 3
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1) + 0.1 * rng.standard_normal(n)
+    th = 10 ** rng.uniform(-0.5, 1.0, size=(12, d))
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=12)
+    r = ev.eval_batch(th)
+    f = ref_fast.eval_batch(X, y, th, 1.95, threads=0)
+    assert np.array_equal(r["jitter"], f["jitter"])
+    assert np.all(np.abs(r["neg2"] - f["neg2"]) <= 1e-9 * np.abs(f["neg2"]) + 1e-9)
+    assert rel(r["mu"], f["mu"]) < 1e-8 and rel(r["sigma2"], f["sigma2"]) < 1e-8
+    ev.close()
