@@ -84,22 +84,29 @@ def sharded_fit(data: g.Dataset, cfg: g.FitConfig,
 
 
 def sharded_predict(model: g.GpModel, Xtest: np.ndarray, device="cpu",
-                    predict_fn=None) -> np.ndarray:
-    """Predictions sharded by test point across ranks, gathered in order on every rank."""
+                    predict_fn=None, with_mse: bool = False):
+    """Predictions sharded by test point across ranks (each GPU predicts N/G
+    points), gathered in order on every rank. with_mse: (yhat, mse), gathered in the same
+    all-gather as (yhat, mse) pairs."""
     import torch
     import torch.distributed as dist
     world, rank = dist.get_world_size(), dist.get_rank()
     N = Xtest.shape[0]
     lo, hi = shard_range(N, world, rank)
-    predict_fn = predict_fn or (lambda X: g.predict(model, X))
-    local = predict_fn(Xtest[lo:hi]) if hi > lo else np.empty(0)
+    cols = 2 if with_mse else 1
+    if predict_fn is None:
+        predict_fn = (lambda X: g.predict(model, X, with_mse=True)) if with_mse else (lambda X: g.predict(model, X))
+    local = predict_fn(Xtest[lo:hi]) if hi > lo else None
     per = math.ceil(N / world)
-    buf = torch.full((per,), float("nan"), dtype=torch.float64, device=device)
+    buf = torch.full((per, cols), float("nan"), dtype=torch.float64, device=device)
     if hi > lo:
-        buf[: hi - lo] = torch.from_numpy(np.asarray(local, dtype=np.float64)).to(device)
+        arr = np.stack([np.asarray(v, dtype=np.float64) for v in local], 1) if with_mse else \
+            np.asarray(local, dtype=np.float64)[:, None]
+        buf[: hi - lo] = torch.from_numpy(arr).to(device)
     parts = [torch.empty_like(buf) for _ in range(world)]
     dist.all_gather(parts, buf)
-    return torch.cat(parts, 0)[:N].cpu().numpy()
+    out = torch.cat(parts, 0)[:N].cpu().numpy()
+    return (out[:, 0].copy(), out[:, 1].copy()) if with_mse else out[:, 0].copy()
 
 
 def sharded_argmin(values_local: np.ndarray, slot_offset: int, device="cpu"):

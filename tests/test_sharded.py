@@ -86,8 +86,11 @@ def _worker(rank, world, port, out_dir, n):
     alpha = orc.solve_upper(L, orc.solve_lower(L, y - res["mu"]))
     yhat = sharded_predict(None, Xt, predict_fn=lambda Xs: orc.predict(X, res["theta"], 1.95,
                                                                      res["mu"], alpha, Xs))
+    yhat2, mse = sharded_predict(None, Xt, with_mse=True, predict_fn=lambda Xs: (
+        orc.predict(X, res["theta"], 1.95, res["mu"], alpha, Xs),
+        orc.kriging_mse(X, res["theta"], 1.95, res["sigma2"], L, Xs)))
     np.savez(os.path.join(out_dir, f"rank{rank}.npz"), theta=res["theta"], neg2=res["neg2"],
-             trace=res["trace_genes"], calls=np.array(calls), yhat=yhat)
+             trace=res["trace_genes"], calls=np.array(calls), yhat=yhat, yhat2=yhat2, mse=mse)
     dist.destroy_process_group()
 
 
@@ -112,6 +115,9 @@ def test_sharded_fit_gloo(orc, tmp_path, world):
     L, ld, jt = orc.factorize(orc.build_corr(X, ref["theta"], 1.95))
     alpha = orc.solve_upper(L, orc.solve_lower(L, y - ref["mu"]))
     assert np.array_equal(outs[0]["yhat"], orc.predict(X, ref["theta"], 1.95, ref["mu"], alpha, Xt))
+    for o in outs:  # (yhat, mse) pairs gathered in order
+        assert np.array_equal(o["yhat2"], outs[0]["yhat"])
+        assert np.array_equal(o["mse"], orc.kriging_mse(X, ref["theta"], 1.95, ref["sigma2"], L, Xt))
 
 
 def _ms_worker(rank, world, port, out_dir):

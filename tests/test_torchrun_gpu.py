@@ -50,6 +50,7 @@ def test_sharded_fit_under_torchrun_nccl():
     r = _torchrun(["tools/sharded_fit.py", "512", "3", "16", "3"])
     assert r.returncode == 0, r.stderr[-3000:]
     assert "sharded fit n=512" in r.stdout
+    assert "bitwise equal to the unsharded prediction: True" in r.stdout
 
 
 def _torchrun_n(n, args, env_extra, timeout=900):
