@@ -192,7 +192,10 @@ GPEMU_API int gpemu_ga_status(const gpemu_ga* ga, int* generation, int* done, do
  * sequential single-candidate evaluations. theta_out / neg2_out: the polished incumbent;
  * model_out (nullable) receives the model rebuilt at it when it improved on neg2_fit,
  * else NULL; scalars[4] = {neg2, mu, sigma2, jitter} and alpha[n] (both nullable) are
- * filled for the rebuilt model only. */
+ * filled for the rebuilt model only. With a plan of max_batch >= 8 each coordinate's
+ * decision tree (2 + 2 + 4 points) is evaluated in one batch and the sequential search is
+ * replayed on those records. Batch invariance makes the result, evals_out and the plan's
+ * ledger those of the one-at-a-time search. */
 GPEMU_API int gpemu_refine_fit(gpemu_plan* plan, const double* lo, const double* hi,
                                const double* theta_fit, double neg2_fit, int budget,
                                double* theta_out, double* neg2_out, int* evals_out,

@@ -59,7 +59,7 @@ inline gpemu::BenchReportRow run_bench_cell_accelerated(Context& ctx, const gpem
     FitResult fit = fit_gp_detailed(ev, lo, hi, ga, seed);
     if (cfg.refine) {
       if (single) {  // the polish runs in double whatever the run precision (bench.hpp:300)
-        BatchEvaluator polish(ctx, Xs, data.outputs(), data.d(), kP, 0.0, 1);
+        BatchEvaluator polish(ctx, Xs, data.outputs(), data.d(), kP, 0.0, 8);  // 8: speculative polish
         row.eval_count += refine_fit(ev, fit, lo, hi, 20, &polish);
       } else {
         row.eval_count += refine_fit(ev, fit, lo, hi, 20);

@@ -1285,22 +1285,94 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
   double best_value = neg2_fit;
   int used = 0;
   int rc = GPEMU_OK;
-  auto eval_genes = [&](const std::vector<double>& genes) -> double {
-    for (int k = 0; k < d; ++k) theta[k] = std::pow(10.0, genes[k]);
+  constexpr double kInvPhi = 0.6180339887498949;
+  constexpr double kHalfWidth = 0.25;  // log10 units around the incumbent
+  // the two golden-section moves (bench.hpp:302-383), shared by the polish and its speculation
+  auto move_left = [&](double& a, double& b, double& x1, double& x2) {
+    b = x2;
+    x2 = x1;
+    x1 = b - kInvPhi * (b - a);
+    return x1;
+  };
+  auto move_right = [&](double& a, double& b, double& x1, double& x2) {
+    a = x1;
+    x1 = x2;
+    x2 = a + kInvPhi * (b - a);
+    return x2;
+  };
+  // Speculation: a coordinate's polish is 2 evaluations plus 2 golden-section steps, each
+  // step choosing between two points known in advance, so the 2 + 2 + 4 points of its
+  // decision tree are evaluated in ONE batch and the sequential algorithm below replays
+  // against those records. Batch invariance makes every record bitwise the value a B=1
+  // evaluation returns, so theta, -2logL and the evaluation count are the sequential
+  // polish's; only the points the replay visits count (the plan's ledger is restored to
+  // that count). Needs 8 slots; smaller plans evaluate one candidate at a time.
+  const bool spec = pl->max_batch >= 8;
+  const uint64_t led_r = pl->r_builds, led_f = pl->factorizations, led_s = pl->solves;
+  double sp_x[8], sp_v[8];
+  int sp_n = 0, sp_k = -1;
+  auto speculate = [&](int k, double a, double b, double x1, double x2) {
+    double pts[8];
+    pts[0] = x1;
+    pts[1] = x2;
+    double aL = a, bL = b, x1L = x1, x2L = x2, aR = a, bR = b, x1R = x1, x2R = x2;
+    pts[2] = move_left(aL, bL, x1L, x2L);
+    pts[3] = move_right(aR, bR, x1R, x2R);
+    {
+      double a2 = aL, b2 = bL, y1 = x1L, y2 = x2L;
+      pts[4] = move_left(a2, b2, y1, y2);
+    }
+    {
+      double a2 = aL, b2 = bL, y1 = x1L, y2 = x2L;
+      pts[5] = move_right(a2, b2, y1, y2);
+    }
+    {
+      double a2 = aR, b2 = bR, y1 = x1R, y2 = x2R;
+      pts[6] = move_left(a2, b2, y1, y2);
+    }
+    {
+      double a2 = aR, b2 = bR, y1 = x1R, y2 = x2R;
+      pts[7] = move_right(a2, b2, y1, y2);
+    }
+    std::vector<double> th((size_t)8 * d);
+    for (int i = 0; i < 8; ++i)
+      for (int q = 0; q < d; ++q) th[(size_t)i * d + q] = std::pow(10.0, q == k ? pts[i] : best[q]);
+    ck(cudaMemcpyAsync(pl->theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice, s),
+       "H2D theta");
+    rc = run_batch(pl, 8);
+    if (rc) return;
+    download_records(pl, 8);
+    for (int i = 0; i < 8; ++i) {
+      sp_x[i] = pts[i];
+      sp_v[i] = pl->h_out[(size_t)i * REC_SIZE + REC_NEG2];
+    }
+    sp_n = 8;
+    sp_k = k;
+  };
+  auto eval_genes = [&](const std::vector<double>& genes, int k) -> double {
     ++used;
-    ck(cudaMemcpyAsync(pl->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
-    rc = run_batch(pl, 1);
-    if (rc) return INFINITY;
-    download_records(pl, 1);
-    const double v = pl->h_out[REC_NEG2];
+    double v = INFINITY;
+    int hit = -1;
+    if (sp_k == k)
+      for (int i = 0; i < sp_n && hit < 0; ++i)
+        if (sp_x[i] == genes[k]) hit = i;
+    if (hit >= 0) {
+      v = sp_v[hit];
+    } else {
+      for (int q = 0; q < d; ++q) theta[q] = std::pow(10.0, genes[q]);
+      ck(cudaMemcpyAsync(pl->theta.p, theta.data(), d * sizeof(double), cudaMemcpyHostToDevice, s),
+         "H2D theta");
+      rc = run_batch(pl, 1);
+      if (rc) return INFINITY;
+      download_records(pl, 1);
+      v = pl->h_out[REC_NEG2];
+    }
     if (v < best_value) {
       best_value = v;
       best = genes;
     }
     return v;
   };
-  constexpr double kInvPhi = 0.6180339887498949;
-  constexpr double kHalfWidth = 0.25;  // log10 units around the incumbent
   int k = 0;
   while (used < budget) {
     g = best;
@@ -1308,32 +1380,36 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
     double b = std::min(std::log10(hi[k]), best[k] + kHalfWidth);
     double x1 = b - kInvPhi * (b - a);
     double x2 = a + kInvPhi * (b - a);
+    sp_k = -1;
+    if (spec && budget - used >= 2) {
+      speculate(k, a, b, x1, x2);
+      if (rc) return rc;
+    }
     g[k] = x1;
-    double f1 = eval_genes(g);
+    double f1 = eval_genes(g, k);
     if (rc) return rc;
     if (used >= budget) break;
     g[k] = x2;
-    double f2 = eval_genes(g);
+    double f2 = eval_genes(g, k);
     if (rc) return rc;
     for (int step = 0; step < 2 && used < budget; ++step) {
       if (f1 <= f2) {
-        b = x2;
-        x2 = x1;
         f2 = f1;
-        x1 = b - kInvPhi * (b - a);
-        g[k] = x1;
-        f1 = eval_genes(g);
+        g[k] = move_left(a, b, x1, x2);
+        f1 = eval_genes(g, k);
       } else {
-        a = x1;
-        x1 = x2;
         f1 = f2;
-        x2 = a + kInvPhi * (b - a);
-        g[k] = x2;
-        f2 = eval_genes(g);
+        g[k] = move_right(a, b, x1, x2);
+        f2 = eval_genes(g, k);
       }
       if (rc) return rc;
     }
     k = (k + 1) % d;
+  }
+  if (spec) {  // the ledger counts the polish's evaluations, not the speculative extras
+    pl->r_builds = led_r + used;
+    pl->factorizations = led_f + used;
+    pl->solves = led_s + 2 * (uint64_t)used;
   }
   for (int q = 0; q < d; ++q) theta[q] = std::pow(10.0, best[q]);
   if (theta_out) std::copy(theta.begin(), theta.end(), theta_out);

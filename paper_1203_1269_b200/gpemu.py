@@ -667,7 +667,12 @@ class ProfileEvaluator:
 
 def neg2_log_profile(theta, data: Dataset, cfg: FitConfig, backend: Backend) -> ProfileEval:
     """likelihood.hpp:161-166."""
-    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=1)
+    # 8 slots let the polish evaluate each coordinate's golden-section decision tree in one
+    # batch (same theta / -2logL / count as one-at-a-time, see gpemu_refine_fit_ex)
+    free, tot = C.c_size_t(), C.c_size_t()
+    _check(lib().gpemu_ctx_mem_info(backend.ctx.handle, C.byref(free), C.byref(tot)))
+    mb = 8 if lib().gpemu_plan_bytes(data.n(), d, 8, 0) <= 0.9 * free.value else 1
+    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=mb)
     try:
         return ev.eval(theta)
     finally:
@@ -842,7 +847,12 @@ def refine_fit(fit: FitResult, data: Dataset, cfg: FitConfig, backend: Backend,
     hi = _f64([b[1] for b in bounds])
     # the polish evaluates in double whatever the run precision (bench.hpp:300-301); the model
     # is rebuilt in the run's precision (bench.hpp:363-382)
-    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=1)
+    # 8 slots let the polish evaluate each coordinate's golden-section decision tree in one
+    # batch (same theta / -2logL / count as one-at-a-time, see gpemu_refine_fit_ex)
+    free, tot = C.c_size_t(), C.c_size_t()
+    _check(lib().gpemu_ctx_mem_info(backend.ctx.handle, C.byref(free), C.byref(tot)))
+    mb = 8 if lib().gpemu_plan_bytes(data.n(), d, 8, 0) <= 0.9 * free.value else 1
+    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=mb)
     rb = ev if parse_precision(cfg.precision) == "double" else ProfileEvaluator(
         data, cfg.p, cfg.nugget, backend, max_batch=1, precision=cfg.precision)
     try:
