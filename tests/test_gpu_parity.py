@@ -619,3 +619,37 @@ def test_eval_tile_boundaries_vs_reference(g, ctx, ref_fast, n):
     assert np.all(np.abs(r["neg2"] - f["neg2"]) <= 1e-9 * np.abs(f["neg2"]) + 1e-9)
     assert rel(r["mu"], f["mu"]) < 1e-8 and rel(r["sigma2"], f["sigma2"]) < 1e-8
     ev.close()
+
+
+@pytest.mark.parametrize("budget", [7, 13, 20])
+def test_refine_speculative_equals_sequential(g, ctx, budget):
+    """gpemu_refine_fit_ex on an 8-slot plan (each coordinate's golden-section decision tree in
+    one batch, replayed) and on a 1-slot plan (one evaluation at a time): bitwise the same
+    polished theta, -2logL, evaluation count and rebuilt model, for budgets that stop
+    mid-coordinate too."""
+    import ctypes as C
+    z = np.load(os.path.join(GOLD, "refine.npz"))
+    X, y, p = z["X_0"], z["y_0"], float(z["p_0"])
+    n, d = X.shape
+    theta_fit = z["theta_fit_0"]
+    data = g.new_dataset(X, y)
+    be = g.Backend(ctx)
+    neg2_fit = float(g.ProfileEvaluator(data, p, 0.0, be, max_batch=1).eval_batch(theta_fit[None, :])["neg2"][0])
+    lo, hi = np.full(d, 1e-6), np.full(d, 12.0)
+    outs = []
+    for mb in (1, 8):
+        ev = g.ProfileEvaluator(data, p, 0.0, be, max_batch=mb)
+        th, sc, al = np.empty(d), np.empty(4), np.empty(n)
+        nv, used, mh = C.c_double(), C.c_int(), C.c_void_p()
+        g._check(g.lib().gpemu_refine_fit_ex(ev.handle, ev.handle, g._p(lo), g._p(hi), g._p(theta_fit),
+                                            neg2_fit, budget, g._p(th), C.byref(nv), C.byref(used),
+                                            C.byref(mh), g._p(sc), g._p(al)))
+        outs.append((th.copy(), nv.value, used.value, bool(mh.value), sc.copy() if mh.value else None,
+                     al.copy() if mh.value else None))
+        if mh.value:
+            g.lib().gpemu_model_destroy(mh)
+        ev.close()
+    (t1, v1, u1, m1, s1, a1), (t8, v8, u8, m8, s8, a8) = outs
+    assert np.array_equal(t1, t8) and v1 == v8 and u1 == u8 == budget and m1 == m8
+    if m1:
+        assert np.array_equal(s1, s8) and np.array_equal(a1, a8)
