@@ -154,6 +154,19 @@ __device__ __forceinline__ void wait_flag(const int* flag, int epoch, int* error
   }
 }
 
+// Spin until *flag >= target (acquire): the slab-progress word of a sub-diagonal tile.
+__device__ __forceinline__ void wait_flag_geq(const int* flag, int target, int* error) {
+  if (ld_acquire_gpu(flag) >= target) return;
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(flag) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > kSpinLimitCycles) {
+      atomicExch(error, 1);
+      return;
+    }
+  }
+}
+
 __device__ __forceinline__ void publish_flag(int* flag, int epoch) {
   __threadfence();
   fence_proxy_async_global();
@@ -483,6 +496,9 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   return true;
 }
 
+// kProgress: release sub-diagonal tiles slab by slab (small, chain-bound launches); the large-
+// launch instantiation carries none of that code.
+template <bool kProgress>
 __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
@@ -528,6 +544,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   // start). Small batches and the last two rounds of tickets do not: a ticket held by a busy
   // CTA would delay a chain that an idle CTA could start at once.
   const bool take_ahead = !ext && ntasks >= 16 * (int)gridDim.x;
+  // Small launches (B=1 models, the 8-candidate refine batches) are bound by each candidate's
+  // serial chain: there the sub-diagonal tile L(j+1, j) is released slab by slab as its TRSM
+  // finishes them, and DIAG(j+1)'s last k-step starts on the first slab. Large launches are
+  // throughput-bound and use the instantiation without the extra barriers.
+  constexpr bool slab_progress = kProgress;
   pr.start();
   while (true) {
     if (tid == 0) {
@@ -636,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (ext) {
             wait_flag(&a.ext_flags[(size_t)It * NT + K], epoch, a.error);
           } else {
-            wait_flag(&flags[j * NT + K], epoch, a.error);
+            if (!(slab_progress && diag && K == j - 1)) wait_flag(&flags[j * NT + K], epoch, a.error);
             if (diag) {
               wait_flag(&flags[NT * NT + K], epoch, a.error);
             } else {
@@ -647,6 +668,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (a.prof) atomicAdd(a.prof + (size_t)gridDim.x * PR_COUNT + (diag ? 128 : 0) + j,
                                 (unsigned long long)(clock64() - tw0));
           pr.lap(PR_PROD_FLAGS);
+        }
+        if (slab_progress && diag && K == j - 1) {
+          // the sub-diagonal tile L(j, j-1) is consumed slab by slab as its OFF task's TRSM
+          // finishes them: progress word flags[(j-1)*NT + j] = 4*epoch + slabs done
+          wait_flag_geq(&flags[(j - 1) * NT + j], 4 * epoch + sq + 1, a.error);
+          fence_proxy_async_global();
         }
         const int stage = itp % kStages;
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
@@ -822,6 +849,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       } else {
         // ------------------------------ OFF -------------------------------
+        const bool sub = slab_progress && I == j + 1;  // feeds DIAG(j+1)'s last k-step
         // L(I,j) = C L(j,j)^-T. L(j,j) arrives by TMA into the (now idle) stage ring;
         // each warp then solves its own 16 rows in registers, 16 columns at a time:
         // (a) in-block substitution (quad shuffles), (b) DMMA update of the columns to
@@ -839,7 +867,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           mbar_wait(ljj_bar, misc->ljj_phase & 1);
         }
         if (tid == 0) pr.lap(PR_OFF_WAIT);
-        const bool run = !skip && (ext || *((volatile int*)&a.status[slot]) == 0);
+        bool run = !skip && (ext || *((volatile int*)&a.status[slot]) == 0);
+        if (sub) run = __syncthreads_and(run);  // uniform: the slab releases below are barriers
         if (run) {
           const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
           // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
@@ -900,6 +929,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               for (int nsub = 0; nsub < 2; ++nsub)
                 __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, w + nsub, lc)),
                        make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1]));
+            if (sub && (cb & 1) && cb < 7) {  // slab cb/2 of L(j+1, j) is final: release it
+              consumer_sync();
+              if (tid == 0) publish_flag(&flags[j * NT + I], 4 * epoch + (cb >> 1) + 1);
+            }
           }
           if (tid == 0) pr.lap(PR_TRSM);
         }
@@ -907,6 +940,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         stamp(2);
         if (tid == 0) {
           if (!skip) ++misc->ljj_phase;  // every consumer passed its ljj wait (consumer_sync above)
+          if (sub) publish_flag(&flags[j * NT + I], 4 * epoch + 4);
           publish_flag(ext ? &a.ext_flags[(size_t)It * NT + j] : &flags[I * NT + j], epoch);
           pr.lap(PR_OFF_STORE);
         }
@@ -923,12 +957,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
 size_t chol_dag_smem_bytes() { return kSmemBytes; }
 
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s) {
-  // per-device attribute: set on every launch (cheap) so multi-device processes are correct
-  cudaFuncSetAttribute(chol_dag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   const int ntasks = a.ext ? a.ext_rt * a.NT : a.nslots * a.NT * (a.NT + 1) / 2;
   const int grid = ntasks < num_sms ? ntasks : num_sms;
+  // the same split as the kernel's take-ahead rule: small launches are chain-bound
+  const bool progress = !a.ext && ntasks < 16 * grid;
+  // per-device attribute: set on every launch (cheap) so multi-device processes are correct
+  cudaFuncSetAttribute(progress ? chol_dag_kernel<true> : chol_dag_kernel<false>,
+                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
   cudaMemsetAsync(a.counter, 0, sizeof(int), s);
-  chol_dag_kernel<<<grid, kThreads, kSmemBytes, s>>>(a);
+  if (progress) {
+    chol_dag_kernel<true><<<grid, kThreads, kSmemBytes, s>>>(a);
+  } else {
+    chol_dag_kernel<false><<<grid, kThreads, kSmemBytes, s>>>(a);
+  }
 }
 
 }  // namespace gpemu_dev
