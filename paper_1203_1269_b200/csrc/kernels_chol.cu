@@ -730,6 +730,14 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             const int ko = (ks ^ lr) << 2;
             const double a0 = -Aw0[ko], a1 = -Aw1[ko];
             const double* BwB = Bw - (warp + 1) * 256;  // slot sl > warp reads n-tile sl - warp - 1
+            // small launches: the border chain runs four columns per k-step ahead of the
+            // DMMAs, hidden under their issue (it is on the serial chain there)
+            if constexpr (kProgress) {
+              const double* ubp = As + SLAB_ELEMS + brow * SLAB;
+#pragma unroll
+              for (int k4 = 0; k4 < 4; ++k4)
+                wacc -= ubp[4 * ks + k4] * As[slab_off(bc, 4 * ks + k4)];
+            }
 #pragma unroll
             for (int sl = 0; sl < 17; ++sl) {
               const bool first = sl <= warp;
@@ -738,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             }
           }
         }
-        if (diag) {
+        if (!kProgress && diag) {
           // border rows: wacc -= sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk], the u_K
           // segment from the stage (broadcast loads)
           const double* ub = As + SLAB_ELEMS + brow * SLAB;
