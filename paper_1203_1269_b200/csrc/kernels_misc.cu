@@ -7,8 +7,8 @@
 //   sigma2_hat_from_parts     likelihood.hpp:63-66
 //   solve_lower/upper_into    backend.hpp:129-153
 // The scalar tail keeps the reference's sequential summation order (one thread
-// per dot) and rounds every product/sum separately: it is O(n) and off the
-// critical path, so bitwise-faithful arithmetic costs nothing measurable.
+// per sum, the four sums concurrent, operands staged in shared memory) and rounds
+// every product/sum separately.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -18,42 +18,51 @@
 
 namespace gpemu_dev {
 
-constexpr int kLogChunk = 2048;
+constexpr int kLogChunk = 1024;
 
+// One block per candidate. Per chunk of kLogChunk rows every thread stages log L_ii, u_i and
+// v_i into shared memory, then the four sequential sums run concurrently from shared memory:
+// the log-sum in warp 1, utu / vtu / vtv in lanes 0-2 of warp 0. Each sum keeps the
+// reference's element order and separate roundings (backend.hpp:111-113, matrix.hpp:64-69).
 __global__ void __launch_bounds__(256) finalize_kernel(
     const double* __restrict__ factors, size_t slot_stride, const double* __restrict__ borders,
     const int* __restrict__ status, const double* __restrict__ jitter, int n, int NT,
     const int* __restrict__ slots, double* __restrict__ out) {
-  __shared__ double logs[kLogChunk];
-  __shared__ double dots[3];
+  __shared__ double logs[kLogChunk], su[kLogChunk], sv[kLogChunk];
+  __shared__ double sums[4];
   const int slot = slots[blockIdx.x];
   const int Npad = NT * TILE;
   const double* fac = factors + (size_t)slot * slot_stride;
   const double* u = borders + (size_t)slot * 2 * Npad;
   const double* v = u + Npad;
   const int st = status[slot];
-  double logsum = 0.0;
   if (st == 0) {
+    double acc = 0.0;  // warp 1 lane 0: logsum; warp 0 lanes 0..2: utu, vtu (v.u), vtv
+    const int t = threadIdx.x;
+    const double* a = t == 2 ? sv : su;
+    const double* b = t == 0 ? su : sv;
     for (int c0 = 0; c0 < n; c0 += kLogChunk) {
       const int cn = min(kLogChunk, n - c0);
-      for (int q = threadIdx.x; q < cn; q += blockDim.x) {
+      for (int q = t; q < cn; q += blockDim.x) {
         const int i = c0 + q;
         logs[q] = log(fac[tile_index(i >> 7, i >> 7) * TILE_ELEMS + elem_off(i & 127, i & 127)]);
+        su[q] = u[i];
+        sv[q] = v[i];
       }
       __syncthreads();
-      if (threadIdx.x == 0)
-        for (int q = 0; q < cn; ++q) logsum = __dadd_rn(logsum, logs[q]);
+      if (t == 32) {
+        for (int q = 0; q < cn; ++q) acc = __dadd_rn(acc, logs[q]);
+      } else if (t < 3) {
+        for (int q = 0; q < cn; ++q) acc = __dadd_rn(acc, __dmul_rn(a[q], b[q]));
+      }
       __syncthreads();
     }
-    if (threadIdx.x < 3) {
-      const double* a = threadIdx.x == 2 ? v : u;
-      const double* b = threadIdx.x == 0 ? u : v;
-      double s = 0.0;
-      for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
-      dots[threadIdx.x] = s;  // 0: utu, 1: vtu (v.u), 2: vtv
-    }
+    if (t < 3) sums[t] = acc;
+    if (t == 32) sums[3] = acc;
     __syncthreads();
   }
+  const double logsum = st == 0 ? sums[3] : 0.0;
+  const double dots[3] = {st == 0 ? sums[0] : 0.0, st == 0 ? sums[1] : 0.0, st == 0 ? sums[2] : 0.0};
   if (threadIdx.x != 0) return;
   double* o = out + (size_t)slot * REC_SIZE;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
