@@ -26,6 +26,13 @@
 //   never re-read L. Operand k-slabs (128 x 32 doubles, 32 KB) are streamed by a
 //   producer warp with cp.async.bulk (TMA) into a 3-stage mbarrier ring; eight
 //   consumer warps run m8n8k4 DMMA on a 128x128 accumulator tile (64x32 per warp).
+//   Two instantiations (launch_chol_dag picks by tickets per CTA):
+//   * chol_dag_kernel<false> (throughput-bound batches such as a GA generation): a CTA takes
+//     its next ticket at mainloop end and bulk-prefetches that task's R tile into L2;
+//   * chol_dag_kernel<true> (B=1 models, refine batches: bound by each candidate's serial
+//     chain): the sub-diagonal tile L(j+1,j) is released slab by slab so DIAG(j+1)'s last
+//     k-step overlaps its TRSM, and the DIAG border chain is interleaved with its DMMAs.
+//   Both produce bitwise the same factor.
 //
 // * chol_simple_kernel -- validation engine: one CTA per candidate, unblocked
 //   right-looking, products and differences rounded separately, so on identical
