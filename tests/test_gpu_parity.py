@@ -653,3 +653,23 @@ def test_refine_speculative_equals_sequential(g, ctx, budget):
     assert np.array_equal(t1, t8) and v1 == v8 and u1 == u8 == budget and m1 == m8
     if m1:
         assert np.array_equal(s1, s8) and np.array_equal(a1, a8)
+
+
+def test_batch_invariance_across_kernel_instantiations(g, ctx):
+    """n=1000 (36 tasks per candidate): a 100-candidate batch runs chol_dag_kernel<false> (take-
+    ahead, >= 16 tickets per CTA), 8 candidates and single evaluations run chol_dag_kernel<true>
+    (slab release of the sub-diagonal tile, interleaved border chain). Both must give bitwise
+    the same record for the same theta."""
+    rng = np.random.default_rng(77)
+    n, d = 1000, 3
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1)
+    th = 10 ** rng.uniform(-1.0, 0.8, size=(100, d))
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=100)
+    big = ev.eval_batch(th)
+    small = ev.eval_batch(th[40:48])
+    one = ev.eval_batch(th[93:94])
+    for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+        assert np.array_equal(big[k][40:48], small[k]), k
+        assert np.array_equal(big[k][93:94], one[k]), k
+    ev.close()
