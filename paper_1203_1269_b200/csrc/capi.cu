@@ -20,9 +20,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
+#include <queue>
 #include <random>
 #include <string>
 #include <vector>
@@ -227,6 +229,8 @@ struct gpemu_plan {
   int precision = GPEMU_PRECISION_DOUBLE;
   DevBuf<float> factors_f, borders_f;  // single precision storage (table: `table`, double)
   DevBuf<unsigned long long> dag_prof;  // optional DAG phase counters
+  DevBuf<int> order;                      // ticket order of large launches (see ticket_order)
+  int order_B = -1;
   std::vector<double> h_jitter;
   std::vector<int> h_slots, h_status_all;
   std::vector<double> h_out;
@@ -282,6 +286,92 @@ namespace {
 
 constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
 
+// Ticket order for a large launch (B candidates x NT(NT+1)/2 tile tasks): a list schedule on
+// P processors with estimated task times (OFF(I,j): ~4 + 18.5 j + 20 us, DIAG(j): ~8 + 10 j +
+// 45 us), ready tasks taken by longest remaining path (bottom level), ties by candidate and
+// tile. Every task is scheduled after its inputs, so the order is topological (the kernel's
+// waits only target lower tickets) and the factor is the same; it only changes which task
+// a free CTA takes next. Packed as bpos << 16 | I << 8 | j (NT <= 256, B < 32768).
+std::vector<int> ticket_order(int B, int NT, int P) {
+  const int T = NT * (NT + 1) / 2;
+  auto id = [](int I, int j) { return I * (I + 1) / 2 + j; };
+  std::vector<double> dur(T), bl(T, 0.0);
+  std::vector<std::vector<int>> succ(T);
+  std::vector<int> ndeps(T, 0), tI(T), tj(T);
+  for (int I = 0; I < NT; ++I)
+    for (int j = 0; j <= I; ++j) {
+      const int t = id(I, j);
+      tI[t] = I;
+      tj[t] = j;
+      dur[t] = I == j ? 53.0 + 10.0 * j : 24.0 + 18.5 * j;
+      for (int K = 0; K < j; ++K) {  // operand tiles (I,K), (j,K)
+        succ[id(j, K)].push_back(t);
+        ++ndeps[t];
+        if (I != j) {
+          succ[id(I, K)].push_back(t);
+          ++ndeps[t];
+        }
+      }
+      if (I != j) {  // L(j,j)
+        succ[id(j, j)].push_back(t);
+        ++ndeps[t];
+      }
+    }
+  for (int j = NT - 1; j >= 0; --j) {  // successors first: later columns, then this column's OFFs
+    for (int I = NT - 1; I >= j; --I) {
+      const int t = id(I == j ? j : I, j);
+      double m = 0.0;
+      for (int u : succ[t]) m = std::max(m, bl[u]);
+      bl[t] = dur[t] + m;
+    }
+  }
+  struct Ready {
+    double bl;
+    int b, t;
+    bool operator<(const Ready& o) const {  // max-heap on bl, then lower candidate, lower tile
+      if (bl != o.bl) return bl < o.bl;
+      if (b != o.b) return b > o.b;
+      return t > o.t;
+    }
+  };
+  struct Done {
+    double time;
+    int b, t;
+    bool operator<(const Done& o) const { return time > o.time; }  // min-heap on time
+  };
+  std::priority_queue<Ready> ready;
+  std::priority_queue<Done> running;
+  std::vector<int> left((size_t)B * T);
+  for (int b = 0; b < B; ++b)
+    for (int t = 0; t < T; ++t) {
+      left[(size_t)b * T + t] = ndeps[t];
+      if (ndeps[t] == 0) ready.push({bl[t], b, t});
+    }
+  std::vector<int> order;
+  order.reserve((size_t)B * T);
+  int free_p = P;
+  double now = 0.0;
+  while (order.size() < (size_t)B * T) {
+    while (free_p > 0 && !ready.empty()) {
+      const Ready r = ready.top();
+      ready.pop();
+      order.push_back(r.b << 16 | tI[r.t] << 8 | tj[r.t]);
+      running.push({now + dur[r.t], r.b, r.t});
+      --free_p;
+    }
+    if (running.empty()) break;  // (cannot happen for a DAG)
+    now = running.top().time;
+    while (!running.empty() && running.top().time <= now) {
+      const Done d = running.top();
+      running.pop();
+      ++free_p;
+      for (int u : succ[d.t])
+        if (--left[(size_t)d.b * T + u] == 0) ready.push({bl[u], d.b, u});
+    }
+  }
+  return order;
+}
+
 void run_chol(gpemu_plan* pl, int nact) {
   DagLaunch a;
   a.factors = pl->factors.p;
@@ -310,6 +400,22 @@ void run_chol(gpemu_plan* pl, int nact) {
   } else if (pl->ctx->engine == GPEMU_ENGINE_SIMPLE) {
     launch_chol_simple(a, pl->ctx->stream);
   } else {
+    const int T = pl->NT * (pl->NT + 1) / 2;
+    const long long ntasks = (long long)nact * T;
+    const int grid = (int)std::min<long long>(ntasks, pl->ctx->num_sms);
+    const char* env = std::getenv("GPEMU_TICKET_ORDER");
+    if (ntasks >= 16LL * grid && nact < (1 << 15) && pl->NT <= 256 && !(env && env[0] == '0')) {
+      if (pl->order_B != nact) {
+        const std::vector<int> ord = ticket_order(nact, pl->NT, grid);
+        pl->order.reserve(ord.size());
+        ck(cudaMemcpyAsync(pl->order.p, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice,
+                           pl->ctx->stream),
+           "H2D ticket order");
+        ck(cudaStreamSynchronize(pl->ctx->stream), "ticket order");
+        pl->order_B = nact;
+      }
+      a.order = pl->order.p;
+    }
     launch_chol_dag(a, pl->ctx->num_sms, pl->ctx->stream);
   }
   pl->ctx->launches += 1;

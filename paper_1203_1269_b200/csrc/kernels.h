@@ -48,6 +48,9 @@ struct DagLaunch {
   // after the GEMM phase, before the publish, and at the end; tickets >= trace_cap skipped
   unsigned long long* trace = nullptr;
   int trace_cap = 0;
+  // optional ticket order (large launches): order[ticket] = bpos << 16 | I << 8 | j, a
+  // topological order from a critical-path list schedule; null = the built-in column order
+  const int* order = nullptr;
 };
 
 void launch_chol_dag(const DagLaunch& a, int num_sms, cudaStream_t s);

@@ -239,6 +239,18 @@ __device__ __forceinline__ void decode_task(int t, int B, int NT, int& bpos, int
   }
 }
 
+// ticket -> task through the launch's order table when it has one
+__device__ __forceinline__ void task_of(const int* order, int t, int B, int NT, int& bpos, int& j, int& I) {
+  if (order) {
+    const int v = __ldg(order + t);
+    bpos = v >> 16;
+    I = (v >> 8) & 255;
+    j = v & 255;
+  } else {
+    decode_task(t, B, NT, bpos, j, I);
+  }
+}
+
 // Offset (tile layout) of the double pair (row r, cols 8 ni + 2 lc + {0,1}) held by a
 // DMMA accumulator fragment.
 __device__ __forceinline__ int acc_off(int r, int ni, int lc) {
@@ -570,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           j = t / a.ext_rt;
           I = t - j * a.ext_rt;  // the extension row tile It
         } else {
-          decode_task(t, B, NT, bpos, j, I);
+          task_of(a.order, t, B, NT, bpos, j, I);
         }
         misc->bpos = bpos;
         misc->I = I;
@@ -781,7 +793,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         misc->next = tn;
         if (tn < ntasks) {
           int bn = 0, jn, In;
-          decode_task(tn, B, NT, bn, jn, In);
+          task_of(a.order, tn, B, NT, bn, jn, In);
           const double* seed = a.factors + (size_t)a.slots[bn] * a.slot_stride + tile_index(In, jn) * TILE_ELEMS;
 #pragma unroll
           for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4) bulk_prefetch_l2(seed + s4 * SLAB_ELEMS, kSlabBytes);

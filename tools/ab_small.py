@@ -33,4 +33,4 @@ def timed(n, d, B, reps=30):
 
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "."
-print(tag, {f"n{n}_B{B}": round(timed(n, d, B), 3) for n, d, B in ((4096, 10, 1), (1024, 6, 1), (1024, 6, 100))})
+print(tag, {f"n{n}_B{B}": round(timed(n, d, B), 3) for n, d, B in ((4096, 10, 1), (1024, 6, 1), (1024, 6, 100), (2048, 6, 64))})

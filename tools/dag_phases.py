@@ -3,7 +3,12 @@ ticket gaps, start->mainloop end (dependency wait + GEMM), epilogue (TRSM/POTRF 
 publish->task end. Fits mainloop time = a + b*K per task kind (K = tile-columns reduced)."""
 import sys
 
+import os
+
 import numpy as np
+
+# tickets are decoded here with the kernel's built-in column order: keep the list-schedule table off
+os.environ["GPEMU_TICKET_ORDER"] = "0"
 
 sys.path.insert(0, "/root/repo")
 import paper_1203_1269_b200.gpemu as g  # noqa: E402

@@ -2,7 +2,12 @@
 distribution of task end times -- how long SMs idle after the ticket counter runs dry."""
 import sys
 
+import os
+
 import numpy as np
+
+# tickets are decoded here with the kernel's built-in column order: keep the list-schedule table off
+os.environ["GPEMU_TICKET_ORDER"] = "0"
 
 sys.path.insert(0, "/root/repo")
 import paper_1203_1269_b200.gpemu as g  # noqa: E402

@@ -4,7 +4,12 @@ Prints, per tile column j of candidate 0: DIAG(j) and OFF(j+1, j) start / GEMM e
 times relative to the launch start, and per-task-kind averages."""
 import sys
 
+import os
+
 import numpy as np
+
+# tickets are decoded here with the kernel's built-in column order: keep the list-schedule table off
+os.environ["GPEMU_TICKET_ORDER"] = "0"
 
 sys.path.insert(0, "/root/repo")
 import paper_1203_1269_b200.gpemu as g  # noqa: E402
