@@ -287,8 +287,9 @@ namespace {
 constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
 
 // Ticket order for a large launch (B candidates x NT(NT+1)/2 tile tasks): a list schedule on
-// P processors with estimated task times (OFF(I,j): ~4 + 18.5 j + 20 us, DIAG(j): ~8 + 10 j +
-// 45 us), ready tasks taken by longest remaining path (bottom level), ties by candidate and
+// P processors with estimated task times (OFF(I,j): ~4 + 18.5 j + 20 us, DIAG(j): ~8 + 18.6 j
+// + 45 us, the measured per-K slopes), ready tasks taken by longest remaining path (bottom
+// level), ties by candidate and
 // tile. Every task is scheduled after its inputs, so the order is topological (the kernel's
 // waits only target lower tickets) and the factor is the same; it only changes which task
 // a free CTA takes next. Packed as bpos << 16 | I << 8 | j (NT <= 256, B < 32768).
@@ -303,7 +304,7 @@ std::vector<int> ticket_order(int B, int NT, int P) {
       const int t = id(I, j);
       tI[t] = I;
       tj[t] = j;
-      dur[t] = I == j ? 53.0 + 10.0 * j : 24.0 + 18.5 * j;
+      dur[t] = I == j ? 53.0 + 18.6 * j : 24.0 + 18.5 * j;
       for (int K = 0; K < j; ++K) {  // operand tiles (I,K), (j,K)
         succ[id(j, K)].push_back(t);
         ++ndeps[t];
