@@ -23,6 +23,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <memory>
+#include <map>
 #include <numeric>
 #include <queue>
 #include <random>
@@ -229,8 +231,9 @@ struct gpemu_plan {
   int precision = GPEMU_PRECISION_DOUBLE;
   DevBuf<float> factors_f, borders_f;  // single precision storage (table: `table`, double)
   DevBuf<unsigned long long> dag_prof;  // optional DAG phase counters
-  DevBuf<int> order;                      // ticket order of large launches (see ticket_order)
-  int order_B = -1;
+  // ticket orders of large launches by batch size (see ticket_order): a GA generation and its
+  // jitter-ladder relaunches alternate between a few sizes
+  std::map<int, std::unique_ptr<DevBuf<int>>> orders;
   std::vector<double> h_jitter;
   std::vector<int> h_slots, h_status_all;
   std::vector<double> h_out;
@@ -406,16 +409,19 @@ void run_chol(gpemu_plan* pl, int nact) {
     const int grid = (int)std::min<long long>(ntasks, pl->ctx->num_sms);
     const char* env = std::getenv("GPEMU_TICKET_ORDER");
     if (ntasks >= 16LL * grid && nact < (1 << 15) && pl->NT <= 256 && !(env && env[0] == '0')) {
-      if (pl->order_B != nact) {
+      auto it = pl->orders.find(nact);
+      if (it == pl->orders.end()) {
+        if (pl->orders.size() >= 8) pl->orders.erase(pl->orders.begin());
         const std::vector<int> ord = ticket_order(nact, pl->NT, grid);
-        pl->order.reserve(ord.size());
-        ck(cudaMemcpyAsync(pl->order.p, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice,
+        auto buf = std::make_unique<DevBuf<int>>();
+        buf->alloc(ord.size());
+        ck(cudaMemcpyAsync(buf->p, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice,
                            pl->ctx->stream),
            "H2D ticket order");
         ck(cudaStreamSynchronize(pl->ctx->stream), "ticket order");
-        pl->order_B = nact;
+        it = pl->orders.emplace(nact, std::move(buf)).first;
       }
-      a.order = pl->order.p;
+      a.order = it->second->p;
     }
     launch_chol_dag(a, pl->ctx->num_sms, pl->ctx->stream);
   }
