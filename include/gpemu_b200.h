@@ -146,6 +146,10 @@ GPEMU_API int gpemu_plan_phase_ms(gpemu_plan* plan, int phase, double* total_ms,
  * kernels_chol.cu PR_*). enable=1 (re)arms and zeroes them; out (nullable) receives the
  * counters accumulated since; enable=0 disarms. */
 GPEMU_API int gpemu_plan_dag_profile(gpemu_plan* plan, int enable, uint64_t* out, size_t out_len);
+/* Diagnostics (host only, no device): the ticket order a large DAG launch of B candidates with
+ * NT tile columns on `procs` CTAs uses (critical-path list schedule). out[B*NT*(NT+1)/2] gets
+ * the packed tasks bpos << 16 | I << 8 | j in ticket order (I == j: DIAG). */
+GPEMU_API int gpemu_ticket_order(int B, int NT, int procs, int* out, size_t out_len);
 
 /* ---- optimizer.hpp / likelihood.hpp fit ------------------------------- */
 typedef struct {

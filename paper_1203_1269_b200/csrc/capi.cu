@@ -1044,6 +1044,18 @@ int gpemu_plan_phase_ms(gpemu_plan* pl, int phase, double* total_ms, int* launch
   GPEMU_GUARD_END
 }
 
+int gpemu_ticket_order(int B, int NT, int procs, int* out, size_t out_len) {
+  GPEMU_GUARD_BEGIN
+  if (B < 1 || B >= (1 << 15) || NT < 1 || NT > 256 || procs < 1 || !out)
+    return set_error(GPEMU_VALIDATION, "ticket_order: bad arguments");
+  const size_t need = (size_t)B * NT * (NT + 1) / 2;
+  if (out_len < need) return set_error(GPEMU_VALIDATION, "ticket_order: out needs %zu entries", need);
+  const std::vector<int> ord = ticket_order(B, NT, procs);
+  std::copy(ord.begin(), ord.end(), out);
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
 int gpemu_plan_dag_profile(gpemu_plan* pl, int enable, uint64_t* out, size_t out_len) {
   GPEMU_GUARD_BEGIN
   if (!pl) return set_error(GPEMU_VALIDATION, "null plan");

@@ -76,7 +76,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
     "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
-    "gpemu_ctx_mem_info", "gpemu_plan_bytes",
+    "gpemu_ctx_mem_info", "gpemu_plan_bytes", "gpemu_ticket_order",
 )
 
 
@@ -137,6 +137,7 @@ def lib():
     L.gpemu_plan_set_profiling.argtypes = [_vp, C.c_int]
     L.gpemu_plan_phase_ms.argtypes = [_vp, C.c_int, _dp, _ip]
     L.gpemu_plan_dag_profile.argtypes = [_vp, C.c_int, C.c_void_p, _sz]
+    L.gpemu_ticket_order.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, _sz]
     L.gpemu_fit.argtypes = [_vp, _dp, _dp, C.POINTER(_GaConfigC), C.c_uint64,
                             C.POINTER(_FitResultC), _dp, _dp, _dp, _dp, C.POINTER(_vp)]
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]

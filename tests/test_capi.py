@@ -107,3 +107,25 @@ def test_host_side_reference_names(g):
         g.make_backend("parallel")  # the CPU backends are the oracle, not the product
     with pytest.raises(g.ConfigError):
         g.FitConfig(precision="half") and g.parse_precision("half")
+
+
+@pytest.mark.parametrize("B,NT,procs", [(1, 5, 148), (7, 9, 148), (100, 8, 148), (64, 16, 148), (3, 32, 20)])
+def test_ticket_order_is_topological(g, B, NT, procs):
+    """The list-schedule ticket order of large DAG launches (gpemu_ticket_order, host only) is a
+    permutation of the B*NT(NT+1)/2 tile tasks in which every task comes after its inputs
+    (OFF(I,j): L(I,K), L(j,K) for K < j and L(j,j); DIAG(j): L(j,K) for K < j): the kernel's
+    waits then only target lower tickets, so no launch can deadlock."""
+    T = NT * (NT + 1) // 2
+    out = np.empty(B * T, dtype=np.int32)
+    g._check(g.lib().gpemu_ticket_order(B, NT, procs, out.ctypes.data, out.size))
+    b, I, j = out >> 16, (out >> 8) & 255, out & 255
+    assert len(set(zip(b.tolist(), I.tolist(), j.tolist()))) == B * T
+    assert np.all(j <= I) and np.all(I < NT) and np.all(b < B)
+    pos = {(int(bb), int(ii), int(jj)): t for t, (bb, ii, jj) in enumerate(zip(b, I, j))}
+    for (bb, ii, jj), t in pos.items():
+        for K in range(jj):
+            assert pos[(bb, jj, K)] < t
+            if ii != jj:
+                assert pos[(bb, ii, K)] < t
+        if ii != jj:
+            assert pos[(bb, jj, jj)] < t
