@@ -89,15 +89,58 @@ def make_inputs(args, rank):
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
+    """SM clock / max clock / clock-event reasons sampled every 20 ms during the timed region:
+    NVML in a background thread (in-process, nothing buffered), else an `nvidia-smi -lms`
+    subprocess. One sample is also taken on entry and exit, so a short region still has
+    evidence."""
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
         self.proc = None
+        self.nvml = None
+        self.samples = []  # (sm_mhz, max_mhz, set of reason names)
+        self.lines = []
+
+    def _nvml_sample(self):
+        nv = self.nvml
+        sm = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.handle, nv.NVML_CLOCK_SM)
+        bits = nv.nvmlDeviceGetCurrentClocksEventReasons(self.handle)
+        masks = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                 nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        self.samples.append((float(sm), float(mx), {n for n, m in zip(self.NAMES, masks) if bits & m}))
+
+    def _loop(self):
+        while not self.stop.wait(0.02):
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        try:
+            import threading
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            try:  # the CUDA device's PCI address (CUDA and NVML may enumerate differently)
+                import torch
+                pr = torch.cuda.get_device_properties(self.index)
+                self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(
+                    f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0")
+            except Exception:
+                self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self._nvml_sample()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -108,7 +151,15 @@ class ClockSampler:
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        if self.nvml is not None:
+            self.stop.set()
+            self.thread.join(timeout=2)
+            try:
+                self._nvml_sample()
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
+            return
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -117,24 +168,21 @@ class ClockSampler:
                 self.proc.kill()
                 out, _ = self.proc.communicate()
             self.lines = [l for l in out.splitlines() if l.strip()]
-
-    def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for l in getattr(self, "lines", []):
+        for l in self.lines:
             f = [x.strip() for x in l.split(",")]
             try:
-                sm.append(float(f[0]))
-                mx = max(mx, float(f[1]))
+                self.samples.append((float(f[0]), float(f[1]),
+                                     {n for n, v in zip(self.NAMES, f[3:7]) if v.lower() == "active"}))
             except (ValueError, IndexError):
                 continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
+
+    def summary(self):
+        if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = set().union(*(r for _, _, r in self.samples))
+        return {"sm_mhz": statistics.median(s for s, _, _ in self.samples),
+                "sm_max_mhz": max(m for _, m, _ in self.samples), "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "nvml" if self.nvml is not None else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------- reference arm
