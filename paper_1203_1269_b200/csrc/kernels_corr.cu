@@ -13,6 +13,8 @@
 // exp/log are CUDA libdevice (<= 1 ulp from glibc): R matches to ~1e-16, not bitwise.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "fastmath.cuh"
 #include "kernels.h"
 #include "layout.cuh"
@@ -159,7 +161,11 @@ void launch_assemble(const double* table, const double* theta, const double* y, 
   const int Npad = NT * TILE;
   border_init_kernel<<<dim3((Npad + 255) / 256 < 32 ? (Npad + 255) / 256 : 32, nslots), 256, 0, s>>>(
       y, n, Npad, slots, borders, status);
-  const dim3 grid(num_tiles(NT), 8);
+  // at least ~8 blocks per SM on small designs (n=200 has 3 tiles: 24 blocks with a fixed 8),
+  // at most one element per thread per slot chunk (TILE_ELEMS / 256 = 64)
+  const int tiles = num_tiles(NT);
+  const int gy = std::min(64, std::max(8, (1184 + tiles - 1) / tiles));
+  const dim3 grid(tiles, gy);
   // theta entries beyond d are zero in shared memory, so a looser bound is only slower
 #define GPEMU_ASM(D) \
   launch_asm<D>(grid, s, table, theta, n, d, nugget, NT, slots, nslots, jitter, factors, slot_stride, status)
