@@ -1,17 +1,19 @@
 #!/usr/bin/env python
 """bench.py -- -2logL evaluations/s on the B200 engine (BASELINE.json metric, config C3).
 
-A step = one pass of the hot path over one batch: B=100 theta candidates (one GA
-generation) through ProfileEvaluator::eval semantics (likelihood.hpp:108-141):
-R assembly (K1), jitter-ladder Cholesky with the bordered solves (K2), deviance (K3).
-Weak scaling: every rank evaluates its own 100-candidate batch (candidates are
-independent; no data-path collective). Inputs (design table, thetas) are resident in
-HBM when the timed region starts; the per-step working set (100 x 69 MB factor tiles)
-is far larger than L2, so no extra flush is needed.
+A step = one pass of the hot path over one GA generation: 100 theta candidates through
+ProfileEvaluator::eval semantics (likelihood.hpp:108-141): R assembly (K1), jitter-ladder
+Cholesky with the bordered solves (K2), deviance (K3). Multi-GPU (one rank per GPU) is STRONG
+scaling, as config C3 describes it: the generation's 100 candidates are split into contiguous
+ranges of ceil(100/N) per rank (optimizer.hpp:86-92); value = 100 x steps / max-over-ranks
+time. With N > 1 the line also carries `weak` (every rank its own 100 candidates) and the
+sharded GA fit's wall time. Inputs (design table, thetas) are resident in HBM when the timed
+region starts; the per-step working set (100 x 69 MB factor tiles) is far larger than L2, so
+no extra flush is needed.
 
-  python bench.py [--gpus N --steps K --warmup W]          # our arm
-  python bench.py --impl reference [...]                    # the reference CPU path
-  torchrun --nproc-per-node N bench.py --gpus N ...         # multi-GPU (one rank per GPU)
+  python bench.py [--gpus N --steps K --warmup W] [--config c3|c2|c4]   # our arm
+  python bench.py --impl reference [...]                                 # the reference CPU path
+  torchrun --nproc-per-node N bench.py --gpus N ...                      # one rank per GPU
 """
 from __future__ import annotations
 
@@ -29,7 +31,12 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "-2logL evals/sec at n=4096,d=10 (C3: batch of 100 thetas per GPU per step)"
+METRIC = "-2logL evals/sec at n=4096,d=10 (C3: one GA generation of 100 thetas per step, sharded over the GPUs)"
+CONFIGS = {  # BASELINE.json configs with a batched-deviance workload
+    "c3": dict(n=4096, d=10, p=1.95, nugget=0.0, batch=100),
+    "c2": dict(n=2048, d=6, p=1.95, nugget=0.0, batch=64),
+    "c4": dict(n=16384, d=20, p=1.9, nugget=1e-8, batch=100),
+}
 UNIT = "evals/s"
 FP64_PEAK_FALLBACK = 37.0  # TFLOP/s, DMMA m8n8k4 measured on this pool (profiles/fp64_peak.json)
 
@@ -40,11 +47,13 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     # (long names: torchrun would take --n / --d / --p as abbreviations of its own options)
-    ap.add_argument("--size", dest="n", type=int, default=4096)
-    ap.add_argument("--dims", dest="d", type=int, default=10)
-    ap.add_argument("--power", dest="p", type=float, default=1.95)
-    ap.add_argument("--batch", type=int, default=100)
+    ap.add_argument("--size", dest="n", type=int, default=None)
+    ap.add_argument("--dims", dest="d", type=int, default=None)
+    ap.add_argument("--power", dest="p", type=float, default=None)
+    ap.add_argument("--nugget", type=float, default=None)
+    ap.add_argument("--batch", type=int, default=None, help="candidates per step (global)")
     ap.add_argument("--seed", type=int, default=20120306)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
@@ -52,7 +61,14 @@ def parse():
     ap.add_argument("--no-single", action="store_true",
                     help="skip the informational single-precision (FP32 engine) rate")
     ap.add_argument("--cpu-sample", type=int, default=0, help="evals in the CPU sample (0: auto)")
-    return ap.parse_args()
+    ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling leg")
+    ap.add_argument("--no-latency", action="store_true",
+                    help="skip the B=1 / model-build latency leg")
+    a = ap.parse_args()
+    for k, v in CONFIGS[a.config].items():
+        if getattr(a, k) is None:
+            setattr(a, k, v)
+    return a
 
 
 # ----------------------------------------------------------------- inputs
@@ -78,13 +94,22 @@ def lhs_thetas(d, count, rng, lo=1e-6, hi=12.0):
     return 10.0 ** (math.log10(lo) + (math.log10(hi) - math.log10(lo)) * g)
 
 
-def make_inputs(args, rank):
+def make_inputs(args, rank=0):
+    """Design, response and the per-step theta batches. make_inputs(args, 0) gives the global
+    generations every rank shards (strong scaling); rank r's own batches feed the weak leg."""
     rng = np.random.default_rng(args.seed)
     X = random_lhd(args.n, args.d, rng)
     y = smooth_response(X)
     trng = np.random.default_rng(args.seed + 1000 * (rank + 1))
     batches = [lhs_thetas(args.d, args.batch, trng) for _ in range(max(args.steps, args.warmup, 1))]
     return X, y, batches
+
+
+def shard(B, world, rank):
+    """Contiguous candidate range of `rank`: ceil(B/world) per rank (sharded.shard_range)."""
+    per = -(-B // world)
+    lo = min(B, rank * per)
+    return lo, min(B, lo + per)
 
 
 # ----------------------------------------------------------------- clocks
@@ -200,13 +225,13 @@ def run_reference_arm(args, rank, world):
         return {"impl": "reference", "unavailable": "oracle/_ref/libgpemu_ref_fast.so not built"}
     ref = RefLib(fast=True)
     X, y, batches = make_inputs(args, 0)
-    per_step = args.cpu_sample or 4
+    per_step = args.cpu_sample or (4 if args.n <= 4096 else 1)
     th = batches[0]
-    ref.eval_batch_timed(X, y, th[:1], args.p)  # page-in; the plan is excluded from timing below
+    ref.eval_batch_timed(X, y, th[:1], args.p, args.nugget)  # page-in; the plan is excluded below
     evals, secs, plan_s = 0, 0.0, 0.0
     for s in range(args.warmup + args.steps):
         sl = th[(s * per_step) % len(th):(s * per_step) % len(th) + per_step]
-        _, sp, se = ref.eval_batch_timed(X, y, sl, args.p, threads=0)
+        _, sp, se = ref.eval_batch_timed(X, y, sl, args.p, args.nugget, threads=0)
         if s >= args.warmup:
             evals += len(sl)
             secs += se
@@ -215,7 +240,7 @@ def run_reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": bench_config(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
@@ -230,11 +255,13 @@ def run_reference_arm(args, rank, world):
 def bench_config(args, world):
     """The workload description both arms print (the reference arm runs the same config)."""
     n, B = args.n, args.batch
-    return {"workload": f"C3: n={n}, d={args.d}, p={args.p}; {B} theta candidates per GPU "
-                        "per step (one GA generation); random LHD design, smooth_response y, "
+    lo, hi = shard(B, world, 0)
+    return {"workload": f"{args.config.upper()}: n={n}, d={args.d}, p={args.p}, nugget={args.nugget}; "
+                        f"one GA generation of {B} theta candidates per step, split over the GPUs "
+                        f"({hi - lo} per GPU at N={world}); random LHD design, smooth_response y, "
                         "thetas from the GA's LHS over the log10 box [1e-6, 12]^d",
-            "n": n, "d": args.d, "p": args.p, "batch_per_gpu": B, "global_batch": B * world,
-            "parallelism": f"candidate sharding x{world} (weak)",
+            "n": n, "d": args.d, "p": args.p, "nugget": args.nugget, "global_batch": B,
+            "batch_per_gpu": hi - lo, "parallelism": f"candidate sharding x{world} (strong)",
             "l2": "inputs larger than L2 (per-step working set ~%.1f GB)" % (
                 B * (n / 128) * (n / 128 + 1) / 2 * 128 * 128 * 8 / 1e9)}
 
@@ -260,95 +287,164 @@ def max_over_ranks(x, dev):
     return float(t.item())
 
 
+def barrier(dist):
+    if dist is not None:
+        dist.barrier()
+
+
+def timed_steps(step, steps, stream, dev, dist, clk=None):
+    """Device time of `steps` calls of step(s), bracketed by barrier + synchronize, max over
+    ranks."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    barrier(dist)
+    e0.record(stream)
+    for s in range(steps):
+        step(s)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier(dist)
+    ms = e0.elapsed_time(e1)
+    return max_over_ranks(ms, dev) if dist is not None else ms
+
+
 def run_ours(args, rank, world, local_rank):
     import torch
     import paper_1203_1269_b200.gpemu as g
     local_rank = rank_device(local_rank)
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    X, y, batches = make_inputs(args, rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+    X, y, batches = make_inputs(args, 0)  # the global generations (same on every rank)
+    B = args.batch
+    lo, hi = shard(B, world, rank)
+    Bl = hi - lo
     ctx = g.Context(local_rank, "dag")
     stream = torch.cuda.current_stream(dev)
     ctx.set_stream(stream.cuda_stream)
     be = g.Backend(ctx)
-    ev = g.ProfileEvaluator(g.new_dataset(X, y), args.p, 0.0, be, max_batch=args.batch)
-    B = args.batch
-    d_th = [torch.from_numpy(b).to(dev) for b in batches]
-    d_out = torch.empty(B * 8, dtype=torch.float64, device=dev)
+    data = g.new_dataset(X, y)
+    ev = g.ProfileEvaluator(data, args.p, args.nugget, be, max_batch=max(1, Bl))
+    d_th = [torch.from_numpy(np.ascontiguousarray(b[lo:hi])).to(dev) for b in batches]
+    d_out = torch.empty(max(1, Bl) * 8, dtype=torch.float64, device=dev)
 
     def step(s):
-        ev.eval_batch_device(d_th[s % len(d_th)].data_ptr(), B, d_out.data_ptr())
+        if Bl:
+            ev.eval_batch_device(d_th[s % len(d_th)].data_ptr(), Bl, d_out.data_ptr())
 
     for s in range(args.warmup):
         step(s)
-    torch.cuda.synchronize(dev)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.barrier()
     ev.set_profiling(True)
     launches0 = ctx.launch_count
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clk:
-        torch.cuda.synchronize(dev)
-        if dist is not None:
-            dist.barrier()
-        e0.record(stream)
-        for s in range(args.steps):
-            step(s)
-        e1.record(stream)
-        torch.cuda.synchronize(dev)
-        if dist is not None:
-            dist.barrier()
-    ms = e0.elapsed_time(e1)
+        ms_max = timed_steps(step, args.steps, stream, dev, dist)
     launches = ctx.launch_count - launches0
     chol_ms, chol_n = ev.phase_ms(1)
     asm_ms, _ = ev.phase_ms(0)
     fin_ms, _ = ev.phase_ms(2)
     ev.set_profiling(False)
-    rec = d_out.view(B, 8).cpu().numpy()
-    status = rec[:, 5]
-    ms_max = max_over_ranks(ms, dev) if dist is not None else ms
-    value = world * B * args.steps / (ms_max / 1e3)
+    rec = d_out.view(-1, 8)[:Bl].cpu().numpy()
+    value = B * args.steps / (ms_max / 1e3)
 
     # ---- e2e: the public API with pinned host buffers (H2D thetas, D2H records) ----
     e2e = None
     if not args.no_e2e:
-        h_th = [torch.from_numpy(b).pin_memory() for b in batches]
-        outs = {k: torch.empty(B, dtype=torch.float64).pin_memory()
+        h_th = [torch.from_numpy(np.ascontiguousarray(b[lo:hi])).pin_memory() for b in batches]
+        outs = {k: torch.empty(max(1, Bl), dtype=torch.float64).pin_memory()
                 for k in ("neg2", "mu", "sigma2", "jitter", "log_det")}
-        st = torch.empty(B, dtype=torch.int32).pin_memory()
+        st = torch.empty(max(1, Bl), dtype=torch.int32).pin_memory()
         L = g.lib()
 
         def api_step(s):
+            if not Bl:
+                return
             th = h_th[s % len(h_th)]
             dp = lambda t: g.C.cast(g._vp(t.data_ptr()), g._dp)  # noqa: E731
-            g._check(L.gpemu_eval_batch(ev.handle, dp(th), B,
+            g._check(L.gpemu_eval_batch(ev.handle, dp(th), Bl,
                                         *[dp(outs[k]) for k in
                                           ("neg2", "mu", "sigma2", "jitter", "log_det")],
                                         g.C.cast(g._vp(st.data_ptr()), g._ip)))
         for s in range(args.warmup):
             api_step(s)
-        torch.cuda.synchronize(dev)
-        if dist is not None:
-            dist.barrier()
-        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        for s in range(args.steps):
-            api_step(s)
-        f1.record(stream)
-        torch.cuda.synchronize(dev)
-        ems = f0.elapsed_time(f1)
-        if dist is not None:
-            ems = max_over_ranks(ems, dev)
-        e2e = {"value": world * B * args.steps / (ems / 1e3), "unit": UNIT,
+        ems = timed_steps(api_step, args.steps, stream, dev, dist)
+        e2e = {"value": B * args.steps / (ems / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": B * args.d * 8, "d2h_bytes_per_step": B * (5 * 8 + 4),
-               "api": "gpemu_eval_batch (C-ABI, host buffers)"}
+               "api": "gpemu_eval_batch (C-ABI, host buffers), each rank its candidate range"}
 
-    out = {"value": value, "ms": ms_max, "status_ok": int(np.sum(status == 0)), "launches": launches,
-           "chol_ms": chol_ms, "chol_launches": chol_n, "asm_ms": asm_ms, "fin_ms": fin_ms,
-           "clocks": clk.summary(), "e2e": e2e, "ev": ev, "be": be, "ctx": ctx, "X": X, "y": y,
-           "batches": batches}
+    out = {"value": value, "ms": ms_max, "status_ok": int(np.sum(rec[:, 5] == 0)),
+           "launches": launches, "chol_ms": chol_ms, "chol_launches": chol_n, "asm_ms": asm_ms,
+           "fin_ms": fin_ms, "clocks": clk.summary(), "e2e": e2e, "ev": ev, "be": be, "ctx": ctx,
+           "X": X, "y": y, "batches": batches, "data": data, "dev": dev, "stream": stream,
+           "dist": dist, "Bl": Bl}
+
+    # ---- weak scaling (N > 1): every rank its own full generation of B candidates ----
+    if world > 1 and not args.no_weak:
+        ev.close()
+        _, _, wb = make_inputs(args, rank)
+        evw = g.ProfileEvaluator(data, args.p, args.nugget, be, max_batch=B)
+        dw = [torch.from_numpy(b).to(dev) for b in wb]
+        dwo = torch.empty(B * 8, dtype=torch.float64, device=dev)
+
+        def wstep(s):
+            evw.eval_batch_device(dw[s % len(dw)].data_ptr(), B, dwo.data_ptr())
+        for s in range(args.warmup):
+            wstep(s)
+        wms = timed_steps(wstep, args.steps, stream, dev, dist)
+        out["weak"] = {"value": world * B * args.steps / (wms / 1e3), "unit": UNIT,
+                       "ms_per_step": wms / args.steps, "batch_per_gpu": B,
+                       "note": "every rank evaluates its own generation of B candidates"}
+        evw.close()
+        out["ev"] = ev = g.ProfileEvaluator(data, args.p, args.nugget, be, max_batch=max(1, Bl))
+    return out
+
+
+def latency_leg(args, r):
+    """B=1 latency at this config (one ProfileEvaluator::eval: refine_fit / model_at_theta
+    batches run like this) and the model build (model_at_theta at theta-hat-like thetas:
+    evaluation + alpha) at C5's n=8192, d=10. Device-timed with events, median of 5."""
+    import torch
+    import paper_1203_1269_b200.gpemu as g
+    dev, stream = r["dev"], r["stream"]
+    ev1 = g.ProfileEvaluator(r["data"], args.p, args.nugget, r["be"], max_batch=1)
+    th = torch.from_numpy(np.ascontiguousarray(r["batches"][0][:8])).to(dev)
+    o = torch.empty(8, dtype=torch.float64, device=dev)
+    times = []
+    for k in range(8):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ev1.eval_batch_device(th[k].data_ptr(), 1, o.data_ptr())
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        if k >= 3:
+            times.append(e0.elapsed_time(e1))
+    ev1.close()
+    out = {"b1_ms": statistics.median(times), "b1_config": f"n={args.n}, d={args.d}, B=1"}
+    # C5 model build: n=8192, d=10 GP design; theta of moderate correlation
+    rng = np.random.default_rng(8192)
+    n5, d5 = 8192, 10
+    X5 = random_lhd(n5, d5, rng)
+    y5 = smooth_response(X5)
+    data5 = g.new_dataset(X5, y5)
+    th5 = 10 ** rng.uniform(0.0, 0.6, d5)
+    ev5 = g.ProfileEvaluator(data5, 1.95, 0.0, r["be"], max_batch=1)
+    L = g.lib()
+    mt, at = [], []
+    for k in range(4):
+        sc, alpha, mh = np.empty(4), np.empty(n5), g._vp()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        g._check(L.gpemu_model_at_theta(ev5.handle, g._p(th5), g.C.byref(mh), g._p(sc), g._p(alpha)))
+        t1 = time.perf_counter()
+        L.gpemu_model_destroy(mh)
+        if k >= 1:
+            mt.append(1e3 * (t1 - t0))
+    ev5.close()
+    out["model_build_ms"] = statistics.median(mt)
+    out["model_build_config"] = ("C5 model: n=8192, d=10, model_at_theta (B=1 evaluation + alpha "
+                                 "by the blocked backward solve), host-timed through the C-ABI")
     return out
 
 
@@ -366,10 +462,10 @@ def fp64_peak():
     p = os.path.join(ROOT, "profiles", "fp64_peak.json")
     if os.path.exists(p):
         try:
-            return float(json.load(open(p))["dmma_tflops"]), "profiles/fp64_peak.json (DMMA m8n8k4 microbench, this pool)"
+            return float(json.load(open(p))["dmma_tflops"]), "profiles/fp64_peak.json (builder-measured DMMA m8n8k4 microbench on this pool; MEASURED_PEAKS.json has no FP64 entry)"
         except (OSError, ValueError, KeyError):
             pass
-    return FP64_PEAK_FALLBACK, "tools/microbench/fp64_peak.cu measurement (37.0 TF DMMA)"
+    return FP64_PEAK_FALLBACK, "tools/microbench/fp64_peak.cu measurement (37.0 TF DMMA, builder-measured)"
 
 
 def main():
@@ -396,8 +492,8 @@ def main():
             dist.init_process_group(DIST_BACKEND)
 
     r = run_ours(args, rank, world, local_rank)
-    B, n = args.batch, args.n
-    flops_per_launch = B * n ** 3 / 3.0  # algorithmic Cholesky flops
+    B, n, Bl = args.batch, args.n, r["Bl"]
+    flops_per_launch = Bl * n ** 3 / 3.0  # algorithmic Cholesky flops
     chol_avg_ms = r["chol_ms"] / max(1, r["chol_launches"])
     achieved = flops_per_launch / (chol_avg_ms / 1e3) / 1e12
     peak, peak_src = fp64_peak()
@@ -405,14 +501,15 @@ def main():
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": r["ms"] / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": bench_config(args, world),
         "roofline": {"kernel": "chol_dag_kernel", "bound": "tensor", "achieved": achieved,
                      "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                     "peak_source": peak_src + " (FP64: MEASURED_PEAKS.json has bf16/HBM only)",
+                     "peak_source": peak_src,
                      "algorithmic_flops_per_launch": flops_per_launch,
                      "avg_launch_ms": chol_avg_ms,
-                     "traffic": traffic.get("bytes_per_launch") if traffic else None},
+                     "traffic": (traffic.get("bytes_per_launch") if traffic and n == 4096 and Bl == 100
+                                 else None)},
         "phases_ms_per_step": {"assemble": r["asm_ms"] / args.steps,
                                "cholesky": r["chol_ms"] / args.steps,
                                "finalize": r["fin_ms"] / args.steps},
@@ -421,12 +518,17 @@ def main():
         "e2e": r["e2e"],
         "candidates_ok": r["status_ok"],
     }
+    if "weak" in r:
+        line["weak"] = r["weak"]
+    dist = r["dist"]
+    # ---- latency: B=1 and the C5 model build ----
+    if rank == 0 and world == 1 and not args.no_latency:
+        line["latency"] = latency_leg(args, r)
     # ---- informational: the same batches on the single-precision engine (Precision::kSingle) ----
     if rank == 0 and world == 1 and not args.no_single:
-        import torch
         import paper_1203_1269_b200.gpemu as g
-        evs = g.ProfileEvaluator(g.new_dataset(r["X"], r["y"]), args.p, 0.0, r["be"],
-                                 max_batch=B, precision="single")
+        evs = g.ProfileEvaluator(r["data"], args.p, args.nugget, r["be"], max_batch=B,
+                                 precision="single")
         for b in r["batches"][:2]:
             evs.eval_batch(b)
         evs.set_profiling(True)
@@ -439,24 +541,43 @@ def main():
         line["single_precision"] = {
             "value": B * args.steps / wall, "unit": UNIT, "chol_ms_per_step": sc_ms / args.steps,
             "note": "informational: FP32 engine (float R/factor/solves, dots in double) on the same "
-                    "batches, host-timed through eval_batch; the headline value is FP64"}
+                    "batches, host-timed through eval_batch; the headline value is FP64. On these "
+                    "GA batches (theta over [1e-6, 12]^d) many candidates climb the float jitter "
+                    "ladder, as in the reference's float instantiation, so FP64 is the faster path"}
         evs.close()
-    # ---- fit wall time (GA 100 x 20 on the same design) ----
-    if rank == 0 and world == 1 and not args.no_fit:
+    # ---- fit wall time (GA 100 x 20 on the same design), sharded over the ranks ----
+    if not args.no_fit:
         import paper_1203_1269_b200.gpemu as g
-        cfg = g.FitConfig(ga=g.GaConfig(population=B, generations=20), seed=1, p=args.p)
-        t = time.time()
-        fr = g.fit_gp_detailed(g.new_dataset(r["X"], r["y"]), cfg, r["be"], evaluator=r["ev"])
-        line["fit"] = {"gpu_wall_s": time.time() - t, "evals": cfg.ga.budget(),
-                       "neg2": fr.model.neg2_log_lik, "ga": f"{B}x20"}
-    # ---- CPU baseline: the reference itself on the host cores (bounded sample) ----
+        cfg = g.FitConfig(ga=g.GaConfig(population=B, generations=20), seed=1, p=args.p,
+                          nugget=args.nugget)
+        if world == 1:
+            t = time.time()
+            fr = g.fit_gp_detailed(r["data"], cfg, r["be"], evaluator=r["ev"])
+            line["fit"] = {"gpu_wall_s": time.time() - t, "evals": cfg.ga.budget(),
+                           "neg2": fr.model.neg2_log_lik, "ga": f"{B}x20",
+                           "api": "gpemu_fit (one device batch per generation)"}
+        else:
+            from paper_1203_1269_b200 import sharded
+            import torch
+            ev = r["ev"]
+            evaluate = lambda th: ev.eval_batch(th)  # noqa: E731
+            barrier(dist)
+            t = time.time()
+            fr = sharded.sharded_fit(r["data"], cfg, evaluate,
+                                     device=r["dev"] if DIST_BACKEND == "nccl" else "cpu")
+            wall = max_over_ranks(time.time() - t, r["dev"])
+            line["fit"] = {"gpu_wall_s": wall, "evals": cfg.ga.budget(), "neg2": float(fr["neg2"]),
+                           "ga": f"{B}x20", "api": "sharded.sharded_fit (contiguous candidate "
+                           "ranges per rank, one NCCL all-gather of 32-B records per generation)"}
+    # ---- CPU baseline: the reference itself on the host cores (bounded sample) + parity ----
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle.oracle import RefLib, ref_available
         if ref_available(fast=True):
+            import paper_1203_1269_b200.gpemu as g
             ref = RefLib(fast=True)
-            S = args.cpu_sample or 16
+            S = args.cpu_sample or (16 if n <= 4096 else 2)
             th = r["batches"][0][:S]
-            neg2, sp, se = ref.eval_batch_timed(r["X"], r["y"], th, args.p, threads=0)
+            neg2, sp, se = ref.eval_batch_timed(r["X"], r["y"], th, args.p, args.nugget, threads=0)
             cpu_v = S / se
             line["cpu_baseline"] = {
                 "value": cpu_v, "unit": UNIT, "cores": cpu_threads(), "kind": "reference",
@@ -464,12 +585,23 @@ def main():
                           f"on all host threads, {se:.1f} s of evals; plan {sp:.2f} s excluded"}
             if "fit" in line:
                 line["fit"]["cpu_wall_s_extrapolated"] = sp + line["fit"]["evals"] / cpu_v
+            # parity of the headline batch itself: the device's step-0 records vs the reference
+            # (gate of tests/test_gpu_parity.py; jitter step and +inf status must be equal)
+            rj = ref.eval_batch(r["X"], r["y"], th, args.p, args.nugget, threads=0)
+            dv = r["ev"].eval_batch(th)
+            fin = np.isfinite(rj["neg2"])
+            rel = np.abs(dv["neg2"][fin] - rj["neg2"][fin]) / np.abs(rj["neg2"][fin])
+            line["parity"] = {
+                "candidates": S, "max_rel_neg2": float(rel.max()) if rel.size else 0.0,
+                "jitter_equal": bool(np.array_equal(dv["jitter"], rj["jitter"])),
+                "inf_status_equal": bool(np.array_equal(np.isinf(dv["neg2"]), np.isinf(rj["neg2"]))),
+                "ref_neg2_bitwise_timed_vs_untimed": bool(np.array_equal(neg2, rj["neg2"])),
+                "against": "oracle/_ref libgpemu_ref_fast.so (the reference's headers, native flags)"}
         else:
             line["cpu_baseline"] = None
     if rank == 0:
         print(json.dumps(line))
     if world > 1:
-        import torch.distributed as dist
         dist.destroy_process_group()
 
 

@@ -68,6 +68,8 @@ GPEMU_API int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream);
 GPEMU_API int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine);
 /* Number of kernels this ctx has launched so far (bench accounting). */
 GPEMU_API uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx);
+/* Streaming multiprocessors of the ctx's device (grid sizing; dag_profile buffer layout). */
+GPEMU_API int gpemu_ctx_num_sms(const gpemu_ctx* ctx);
 
 /* -- correlation.hpp ------------------------------------------------------ */
 /* build_corr_matrix (correlation.hpp:99-146) / CorrelationPlan::build_into (:187-223):
@@ -174,6 +176,22 @@ typedef struct {
 GPEMU_API int gpemu_fit(gpemu_plan* plan, const double* lo, const double* hi, const gpemu_ga_config* ga,
               uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
               double* trace_best, double* trace_genes, gpemu_model** model_out);
+
+/* Candidate sharding over G plans of the same dataset (one per device: gpemu_ctx_create(k),
+ * gpemu_plan_create on it). optimizer.hpp:86-92 lets a generation be evaluated in parallel
+ * (evaluate_population, :116-121); here candidate range k of ceil(P/G) runs on plans[k] from its
+ * own host thread, each plan in chunks of its max_batch, and the records come back in slot
+ * order. No device-to-device traffic: the fit's stash (likelihood.hpp:257-273, strict <,
+ * earliest slot) keeps the winning factor on the device that produced it and the model is
+ * built there. theta-hat, the trace and every record are bitwise those of gpemu_fit on one
+ * plan (batch invariance). Plans must share n, d, X, y, p, nugget and precision. */
+GPEMU_API int gpemu_eval_batch_multi(gpemu_plan* const* plans, int G, const double* theta, size_t B,
+                                     double* neg2, double* mu, double* sigma2, double* jitter,
+                                     double* log_det, int* slot_status);
+GPEMU_API int gpemu_fit_multi(gpemu_plan* const* plans, int G, const double* lo, const double* hi,
+                              const gpemu_ga_config* ga, uint64_t seed, gpemu_fit_result* res,
+                              double* theta_hat, double* alpha, double* trace_best,
+                              double* trace_genes, gpemu_model** model_out);
 
 /* The reference GA (optimizer.hpp:93-187) as a host-only state machine (no device
  * needed): gpemu_ga_thetas gives the current generation's P candidates in theta space

@@ -13,6 +13,7 @@
 //   model_at_theta / predict    likelihood.hpp:216-237, predictor.hpp:20-50
 // There is no CPU fallback: every numeric result comes from the sm_100a kernels.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cfloat>
@@ -29,6 +30,7 @@
 #include <queue>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/gpemu_b200.h"
@@ -57,6 +59,22 @@ struct CudaError {
 
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError{std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+// NVTX ranges (header-only NVTX3: a no-op unless a tool such as nsys / ncu is attached): one per
+// K1-K4 phase launch, per GA generation, per refine polish and per prediction call.
+inline void nvtx_push(const char* name) { nvtxRangePushA(name); }
+inline void nvtx_pop() { nvtxRangePop(); }
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtx_push(name); }
+  ~NvtxRange() { nvtx_pop(); }
+};
+
+// Device -> host copy ordered on `s` (the engine's streams are non-blocking, so a legacy
+// cudaMemcpy is not ordered after their work).
+void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s, const char* what) {
+  ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), what);
+  ck(cudaStreamSynchronize(s), what);
 }
 
 constexpr double kLadder[6] = {0.0, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4};  // backend.hpp:77
@@ -110,11 +128,18 @@ void pool_trim(int dev) {
   ck(cudaMemPoolTrimTo(P.pool, 0), "cudaMemPoolTrimTo");
 }
 
+// A pool allocation. Frees are stream-ordered on the owner's stream (`sp`: the owning
+// context's current stream, bound by own()): every kernel that used the block was issued on
+// that stream before the free, and the pool hands a freed block to the next allocation only
+// after that stream's work reaches the free (the pool's default event-dependency reuse rules),
+// so no device-wide synchronisation is needed. An unbound buffer (no owner) falls back to
+// synchronising its device before the free.
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
   size_t count = 0;
   int dev = -1;
+  const cudaStream_t* sp = nullptr;
   void alloc(size_t c) {
     free();
     if (c == 0) c = 1;
@@ -138,13 +163,15 @@ struct DevBuf {
   }
   void free() {
     if (p) {
-      // cudaFree's implicit device synchronisation, kept: no kernel may still use the block
-      // when the pool hands it to the next allocation
       int cur = -1;
       cudaGetDevice(&cur);
       if (cur != dev) cudaSetDevice(dev);
-      cudaDeviceSynchronize();
-      cudaFreeAsync(p, dev_pool(dev).stream);
+      if (sp) {
+        cudaFreeAsync(p, *sp);
+      } else {
+        cudaDeviceSynchronize();
+        cudaFreeAsync(p, dev_pool(dev).stream);
+      }
       if (cur != dev && cur >= 0) cudaSetDevice(cur);
     }
     p = nullptr;
@@ -152,6 +179,12 @@ struct DevBuf {
   }
   ~DevBuf() { free(); }
 };
+
+// Binds buffers to the stream their users launch on (see DevBuf).
+template <typename... B>
+void own(const cudaStream_t* s, B&... bufs) {
+  ((bufs.sp = s), ...);
+}
 
 // splitmix64 seed derivation (rng.hpp:12-25).
 uint64_t mix64(uint64_t z) {
@@ -217,6 +250,11 @@ struct gpemu_ctx {
   // thousands of them), rebuilt only when n changes.
   gpemu_plan* scratch = nullptr;
   DevBuf<double> scratch_a, scratch_l;
+  // Plans and models free their device buffers on this context's stream, so a context
+  // destroyed while some are alive is finalised when the last of them goes.
+  std::mutex mu;
+  int children = 0;
+  bool closing = false;
 };
 
 struct gpemu_plan {
@@ -234,6 +272,9 @@ struct gpemu_plan {
   // ticket orders of large launches by batch size (see ticket_order): a GA generation and its
   // jitter-ladder relaunches alternate between a few sizes
   std::map<int, std::unique_ptr<DevBuf<int>>> orders;
+  uint64_t data_hash = 0;  // FNV-1a of (n, d, X, y): plans of one dataset on several devices
+  DevBuf<int> trsv_flags, trsv_counter;  // blocked triangular solve (alpha)
+  int trsv_epoch = 0;
   std::vector<double> h_jitter;
   std::vector<int> h_slots, h_status_all;
   std::vector<double> h_out;
@@ -247,6 +288,13 @@ struct gpemu_plan {
     cudaEvent_t a, b;
   };
   std::vector<Mark> marks;
+  void bind() {  // stream-ordered frees on the context's stream (DevBuf)
+    own(&ctx->stream, X, y, table, factors, borders, theta, jitter, out);
+    own(&ctx->stream, status, slots, flags, counter, error);
+    own(&ctx->stream, factors_f, borders_f);
+    own(&ctx->stream, dag_prof, trsv_flags, trsv_counter);
+    for (auto& o : orders) own(&ctx->stream, *o.second);
+  }
   void mark_begin(int kind) {
     if (!profile) return;
     Mark m{kind, nullptr, nullptr};
@@ -283,9 +331,51 @@ struct gpemu_model {
   // predict scratch, grown on demand and reused across calls (no per-call cudaMalloc/Free)
   DevBuf<double> pred_xt, pred_y, pred_mse, pred_part;
   DevBuf<int> pred_bad;
+  void bind() {  // stream-ordered frees on the context's stream (DevBuf)
+    own(&ctx->stream, X, theta_d, alpha, tiles, u, v, ext);
+    own(&ctx->stream, ext_flags, ext_slot, counter, error);
+    own(&ctx->stream, pred_xt, pred_y, pred_mse, pred_part);
+    own(&ctx->stream, pred_bad);
+  }
 };
 
+// Releases a context's stream, scratch and idle pool pages.
+static void ctx_finalize(gpemu_ctx* ctx) {
+  delete ctx->scratch;
+  ctx->scratch_a.free();
+  ctx->scratch_l.free();
+  cudaStreamSynchronize(ctx->stream);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  const int dev = ctx->device;
+  delete ctx;
+  try {  // hand the idle pool pages back to the driver (other CUDA users in the process)
+    pool_trim(dev);
+  } catch (const CudaError&) {
+  }
+}
+
+
 namespace {
+
+void ctx_adopt(gpemu_ctx* c) {
+  std::lock_guard<std::mutex> lock(c->mu);
+  ++c->children;
+}
+
+// Deletes a plan / model, then finalises its context if that was destroyed meanwhile.
+template <typename H>
+void release(H* h) {
+  if (!h) return;
+  gpemu_ctx* c = h->ctx;
+  delete h;
+  if (!c) return;
+  bool fin = false;
+  {
+    std::lock_guard<std::mutex> lock(c->mu);
+    fin = --c->children == 0 && c->closing;
+  }
+  if (fin) ctx_finalize(c);
+}
 
 constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
 
@@ -414,6 +504,7 @@ void run_chol(gpemu_plan* pl, int nact) {
         if (pl->orders.size() >= 8) pl->orders.erase(pl->orders.begin());
         const std::vector<int> ord = ticket_order(nact, pl->NT, grid);
         auto buf = std::make_unique<DevBuf<int>>();
+        own(&pl->ctx->stream, *buf);
         buf->alloc(ord.size());
         ck(cudaMemcpyAsync(buf->p, ord.data(), ord.size() * sizeof(int), cudaMemcpyHostToDevice,
                            pl->ctx->stream),
@@ -431,7 +522,9 @@ void run_chol(gpemu_plan* pl, int nact) {
 // Evaluates slots [0, B) whose thetas are already in pl->theta; runs the jitter
 // ladder (backend.hpp:105-119) on the device, re-assembling R only for the
 // candidates whose factorization failed. Leaves records in pl->out.
-int run_batch(gpemu_plan* pl, size_t B) {
+// With tolerate_nonfinite a slot with a non-finite R entry is left with its status-2 record
+// instead of failing the batch (speculative evaluations the caller may never use).
+int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
   cudaStream_t s = pl->ctx->stream;
   pl->last_B = B;
   pl->last_ladder.assign(B, -1);
@@ -451,6 +544,7 @@ int run_batch(gpemu_plan* pl, size_t B) {
     std::copy(active.begin(), active.end(), pl->h_slots.begin());
     ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), nact * sizeof(int), cudaMemcpyHostToDevice, s),
        "H2D slots");
+    nvtx_push("K1 assemble");
     pl->mark_begin(0);
     if (pl->precision == GPEMU_PRECISION_SINGLE)
       launch_assemble_f32(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
@@ -459,11 +553,15 @@ int run_batch(gpemu_plan* pl, size_t B) {
     else
       launch_assemble(pl->table.p, pl->theta.p, pl->y.p, pl->n, pl->d, pl->nugget, pl->NT,
                       pl->slots.p, nact, pl->jitter.p, pl->factors.p, pl->slot_stride,
-                      pl->borders.p, pl->status.p, s);
+                      pl->borders.p, pl->status.p, pl->ctx->num_sms, s);
     pl->mark_end();
+    nvtx_pop();
+    nvtx_push("K2 cholesky + border solves");
     pl->mark_begin(1);
     run_chol(pl, nact);
     pl->mark_end();
+    nvtx_pop();
+    nvtx_push("K3 finalize");
     pl->mark_begin(2);
     if (pl->precision == GPEMU_PRECISION_SINGLE)
       launch_finalize_f32(pl->factors_f.p, pl->slot_stride, pl->borders_f.p, pl->status.p,
@@ -472,6 +570,7 @@ int run_batch(gpemu_plan* pl, size_t B) {
       launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
                       pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
     pl->mark_end();
+    nvtx_pop();
     pl->ctx->launches += 4;
     ck(cudaGetLastError(), "kernel launch");
     ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, B * sizeof(int), cudaMemcpyDeviceToHost, s),
@@ -481,7 +580,10 @@ int run_batch(gpemu_plan* pl, size_t B) {
     for (int q = 0; q < nact; ++q) {
       const int slot = active[q];
       const int st = pl->h_status_all[slot];
-      if (st == 2) return set_error(GPEMU_NONFINITE, "CorrelationPlan: non-finite correlation value");
+      if (st == 2) {
+        if (tolerate_nonfinite) continue;
+        return set_error(GPEMU_NONFINITE, "CorrelationPlan: non-finite correlation value");
+      }
       if (st == 1) {
         failed.push_back(slot);
       } else {
@@ -491,7 +593,7 @@ int run_batch(gpemu_plan* pl, size_t B) {
     active.swap(failed);
   }
   int err = 0;
-  ck(cudaMemcpy(&err, pl->error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H error");
+  d2h_sync(&err, pl->error.p, sizeof(int), pl->ctx->stream, "D2H error");
   if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
   pl->r_builds += B;
   pl->factorizations += B;
@@ -507,28 +609,35 @@ int download_records(gpemu_plan* pl, size_t B) {
   return GPEMU_OK;
 }
 
-// alpha = (R + jI)^-1 (y - mu 1) on the factor of `slot` (solve_full, backend.hpp:163-169).
+// alpha = (R + jI)^-1 (y - mu 1) on the factor of `slot` (solve_full, backend.hpp:163-169;
+// likelihood.hpp:226-230). The forward half is already in the factor's border rows:
+// L^-1 (y - mu 1) = u - mu v, so one blocked backward solve (kernels_trsv.cu) gives alpha.
+// d_alpha: Npad doubles. Two triangular solves in the Ledger, as the reference's solve_full.
 void solve_alpha(gpemu_plan* pl, int slot, double mu, double* d_alpha) {
+  NvtxRange range("K3 alpha (blocked backward solve)");
   cudaStream_t s = pl->ctx->stream;
-  std::vector<double> hy(pl->n);
-  // rhs is formed on the host from y (an O(n) subtraction, as likelihood.hpp:288).
-  ck(cudaMemcpy(hy.data(), pl->y.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H y");
-  for (int i = 0; i < pl->n; ++i) hy[i] = hy[i] - mu;
-  DevBuf<double> rhs, u;
-  rhs.alloc(pl->n);
-  u.alloc(pl->n);
-  ck(cudaMemcpy(rhs.p, hy.data(), pl->n * sizeof(double), cudaMemcpyHostToDevice), "H2D rhs");
+  pl->trsv_flags.reserve(pl->NT);
+  pl->trsv_counter.reserve(1);
+  if (pl->trsv_epoch == 0)
+    ck(cudaMemsetAsync(pl->trsv_flags.p, 0, pl->NT * sizeof(int), s), "memset trsv flags");
   const double* tiles = pl->factors.p + (size_t)slot * pl->slot_stride;
-  launch_tri_solve(tiles, pl->n, pl->NT, rhs.p, u.p, 0, s);
-  launch_tri_solve(tiles, pl->n, pl->NT, u.p, d_alpha, 1, s);
-  pl->ctx->launches += 2;
+  const double* u = pl->borders.p + (size_t)slot * 2 * pl->Npad;
+  launch_tile_trsv(tiles, pl->NT, u, u + pl->Npad, mu, pl->Npad, d_alpha, 1, pl->trsv_flags.p,
+                   pl->trsv_counter.p, ++pl->trsv_epoch, pl->error.p, pl->ctx->num_sms, s);
+  pl->ctx->launches += 1;
+  ck(cudaGetLastError(), "tile_trsv launch");
+  int err = 0;
+  ck(cudaMemcpyAsync(&err, pl->error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
   ck(cudaStreamSynchronize(s), "solve_alpha");
+  if (err) throw CudaError{"tile_trsv: dependency wait timed out (deadlock guard)"};
   pl->solves += 2;
 }
 
 gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const double* rec) {
   auto* m = new gpemu_model();
+  ctx_adopt(pl->ctx);
   m->ctx = pl->ctx;
+  m->bind();
   m->n = pl->n;
   m->d = pl->d;
   m->NT = pl->NT;
@@ -542,7 +651,7 @@ gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const dou
   cudaStream_t s = pl->ctx->stream;
   m->X.alloc((size_t)pl->n * pl->d);
   m->theta_d.alloc(pl->d);
-  m->alpha.alloc(pl->n);
+  m->alpha.alloc(pl->Npad);  // the blocked solve writes whole 128-row blocks
   m->tiles.alloc(pl->slot_stride);
   m->u.alloc(pl->Npad);
   m->v.alloc(pl->Npad);
@@ -559,8 +668,9 @@ gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const dou
                        cudaMemcpyDeviceToHost, s), "D2H borders");
     ck(cudaStreamSynchronize(s), "borders");
     std::vector<double> hu(hb.begin(), hb.begin() + pl->Npad), hv(hb.begin() + pl->Npad, hb.end());
-    ck(cudaMemcpy(m->u.p, hu.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice), "model u");
-    ck(cudaMemcpy(m->v.p, hv.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice), "model v");
+    // ordered on the ctx stream (a non-blocking stream is not ordered after legacy copies)
+    ck(cudaMemcpyAsync(m->u.p, hu.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice, s), "model u");
+    ck(cudaMemcpyAsync(m->v.p, hv.data(), pl->Npad * sizeof(double), cudaMemcpyHostToDevice, s), "model v");
     launch_alpha_f32(ftiles, pl->n, pl->y.p, m->mu, m->alpha.p, s);
     pl->ctx->launches += 2;
     ck(cudaStreamSynchronize(s), "float model");
@@ -614,6 +724,7 @@ int gpemu_ctx_create(int device, gpemu_ctx** out) {
   c->num_sms = prop.multiProcessorCount;
   ck(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
   c->stream = c->own;
+  own(&c->stream, c->scratch_a, c->scratch_l);
   *out = c;
   return GPEMU_OK;
   GPEMU_GUARD_END
@@ -621,19 +732,21 @@ int gpemu_ctx_create(int device, gpemu_ctx** out) {
 
 int gpemu_ctx_destroy(gpemu_ctx* ctx) {
   if (!ctx) return GPEMU_OK;
-  delete ctx->scratch;
-  if (ctx->own) cudaStreamDestroy(ctx->own);
-  const int dev = ctx->device;
-  delete ctx;
-  try {  // hand the idle pool pages back to the driver (other CUDA users in the process)
-    pool_trim(dev);
-  } catch (const CudaError&) {
+  {
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    if (ctx->children > 0) {  // finalised by the last plan / model
+      ctx->closing = true;
+      return GPEMU_OK;
+    }
   }
+  ctx_finalize(ctx);
   return GPEMU_OK;
 }
 
 int gpemu_ctx_set_stream(gpemu_ctx* ctx, void* stream) {
   if (!ctx) return set_error(GPEMU_VALIDATION, "null ctx");
+  // work (and stream-ordered frees) already issued on the old stream completes first
+  cudaStreamSynchronize(ctx->stream);
   ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
   return GPEMU_OK;
 }
@@ -647,6 +760,7 @@ int gpemu_ctx_set_engine(gpemu_ctx* ctx, int engine) {
 }
 
 uint64_t gpemu_ctx_launch_count(const gpemu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+int gpemu_ctx_num_sms(const gpemu_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
 
 int gpemu_ctx_mem_info(gpemu_ctx* ctx, size_t* free_bytes, size_t* total_bytes) {
   GPEMU_GUARD_BEGIN
@@ -679,6 +793,7 @@ int gpemu_build_corr(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const 
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   DevBuf<double> dX, dT, dR;
   DevBuf<int> bad;
+  own(&ctx->stream, dX, dT, dR, bad);
   dX.alloc(n * d);
   dT.alloc(d);
   dR.alloc(n * n);
@@ -708,6 +823,7 @@ int gpemu_corr_vector(gpemu_ctx* ctx, const double* xstar, const double* X, size
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   DevBuf<double> dX, dT, dS, dR;
   DevBuf<int> bad;
+  own(&ctx->stream, dX, dT, dS, dR, bad);
   dX.alloc(n * d);
   dT.alloc(d);
   dS.alloc(d);
@@ -745,13 +861,14 @@ static int factor_once(gpemu_ctx* ctx, gpemu_plan& pl, const double* dR, double 
   ck(cudaMemcpyAsync(rec, pl.out.p, REC_SIZE * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
   ck(cudaStreamSynchronize(s), "factorize");
   int err = 0;
-  ck(cudaMemcpy(&err, pl.error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+  d2h_sync(&err, pl.error.p, sizeof(int), ctx->stream, "D2H error");
   if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
   return GPEMU_OK;
 }
 
 static void single_slot_plan(gpemu_ctx* ctx, gpemu_plan& pl, size_t n) {
   pl.ctx = ctx;
+  pl.bind();
   pl.n = (int)n;
   pl.NT = (int)((n + TILE - 1) / TILE);
   pl.Npad = pl.NT * TILE;
@@ -853,17 +970,30 @@ static int solve_common(gpemu_ctx* ctx, const double* L, size_t n, const double*
   const int NT = (int)((n + TILE - 1) / TILE);
   cudaStream_t s = ctx->stream;
   DevBuf<double> dL, tiles, db, dx;
+  DevBuf<int> flags, counter, error;
+  own(&ctx->stream, dL, tiles, db, dx);
+  own(&ctx->stream, flags, counter, error);
   dL.alloc(n * n);
   tiles.alloc((size_t)num_tiles(NT) * TILE_ELEMS);
   db.alloc(n);
-  dx.alloc(n);
+  dx.alloc((size_t)NT * TILE);
+  flags.alloc(NT);
+  counter.alloc(1);
+  error.alloc(1);
+  ck(cudaMemsetAsync(flags.p, 0, NT * sizeof(int), s), "memset");
+  ck(cudaMemsetAsync(error.p, 0, sizeof(int), s), "memset");
   ck(cudaMemcpyAsync(dL.p, L, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D L");
   ck(cudaMemcpyAsync(db.p, b, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D b");
   launch_rowmajor_to_tiles(dL.p, (int)n, NT, 0.0, tiles.p, s);
-  launch_tri_solve(tiles.p, (int)n, NT, db.p, dx.p, upper, s);
+  launch_tile_trsv(tiles.p, NT, db.p, nullptr, 0.0, (int)n, dx.p, upper, flags.p, counter.p, 1,
+                   error.p, ctx->num_sms, s);
   ctx->launches += 2;
+  ck(cudaGetLastError(), "solve launch");
+  int err = 0;
   ck(cudaMemcpyAsync(x, dx.p, n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H x");
+  ck(cudaMemcpyAsync(&err, error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
   ck(cudaStreamSynchronize(s), "solve");
+  if (err) return set_error(GPEMU_CUDA, "tile_trsv: dependency wait timed out (deadlock guard)");
   return GPEMU_OK;
   GPEMU_GUARD_END
 }
@@ -903,6 +1033,8 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
   ck(cudaSetDevice(ctx->device), "cudaSetDevice");
   auto* pl = new gpemu_plan();
   pl->ctx = ctx;
+  pl->bind();
+  ctx_adopt(ctx);
   pl->n = (int)n;
   pl->d = (int)d;
   pl->p = p;
@@ -934,8 +1066,20 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
     pl->counter.alloc(1);
     pl->error.alloc(1);
   } catch (const CudaError& e) {
-    delete pl;
+    release(pl);
     return set_error(GPEMU_CUDA, "plan_create: device allocation failed (%s)", e.msg.c_str());
+  }
+  {
+    uint64_t h = 1469598103934665603ull;
+    auto mixb = [&h](const void* p, size_t bytes) {
+      const unsigned char* c = static_cast<const unsigned char*>(p);
+      for (size_t i = 0; i < bytes; ++i) h = (h ^ c[i]) * 1099511628211ull;
+    };
+    mixb(&n, sizeof(n));
+    mixb(&d, sizeof(d));
+    mixb(X, n * d * sizeof(double));
+    mixb(y, n * sizeof(double));
+    pl->data_hash = h;
   }
   cudaStream_t s = ctx->stream;
   ck(cudaMemcpyAsync(pl->X.p, X, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D X");
@@ -960,7 +1104,7 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
 }
 
 int gpemu_plan_destroy(gpemu_plan* plan) {
-  delete plan;
+  release(plan);
   return GPEMU_OK;
 }
 
@@ -1062,13 +1206,13 @@ int gpemu_plan_dag_profile(gpemu_plan* pl, int enable, uint64_t* out, size_t out
   const size_t len = (size_t)pl->ctx->num_sms * 24 + 256 + (size_t)kTraceTasks * 4;
   if (out && pl->dag_prof.p) {
     ck(cudaStreamSynchronize(pl->ctx->stream), "dag_profile");
-    ck(cudaMemcpy(out, pl->dag_prof.p, std::min(out_len, len) * sizeof(uint64_t), cudaMemcpyDeviceToHost),
-       "D2H prof");
+    d2h_sync(out, pl->dag_prof.p, std::min(out_len, len) * sizeof(uint64_t), pl->ctx->stream,
+             "D2H prof");
   }
   if (enable && !pl->dag_prof.p) {
     pl->dag_prof.alloc(len);
   }
-  if (enable) ck(cudaMemset(pl->dag_prof.p, 0, len * sizeof(uint64_t)), "memset prof");
+  if (enable) ck(cudaMemsetAsync(pl->dag_prof.p, 0, len * sizeof(uint64_t), pl->ctx->stream), "memset prof");
   if (!enable) pl->dag_prof.free();
   return GPEMU_OK;
   GPEMU_GUARD_END
@@ -1083,6 +1227,7 @@ int gpemu_plan_last_factor(gpemu_plan* pl, size_t slot, double* L_out, double* l
   cudaStream_t s = pl->ctx->stream;
   if (L_out) {
     DevBuf<double> dL;
+    own(&pl->ctx->stream, dL);
     dL.alloc((size_t)pl->n * pl->n);
     if (pl->precision == GPEMU_PRECISION_SINGLE)
       launch_tiles_f32_to_rowmajor(pl->factors_f.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
@@ -1273,77 +1418,192 @@ int gpemu_ga_status(const gpemu_ga* g, int* generation, int* done, double* best_
   return GPEMU_OK;
 }
 
-int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga_config* gac,
-              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
-              double* trace_best, double* trace_genes, gpemu_model** model_out) {
-  GPEMU_GUARD_BEGIN
-  if (!pl || !lo || !hi || !gac) return set_error(GPEMU_VALIDATION, "fit: null argument");
-  gpemu_ga ga;
-  int rc = ga_setup(&ga, pl->d, lo, hi, gac, seed);
-  if (rc) return rc;
-  const int d = pl->d, P = ga.P;
-  // A generation larger than the plan's slots is evaluated in chunks of max_batch (batch
-  // invariance: a theta's record does not depend on its slot or batch); the stash is kept
-  // chunk by chunk with the reference's rule (strict < in slot order, likelihood.hpp:267), so
-  // the winning factor is saved before a later chunk reuses its slot.
-  const int MB = (int)pl->max_batch;
-  const int stash = MB;  // device slot holding the best factor
-  cudaStream_t s = pl->ctx->stream;
-  std::vector<double> thetas((size_t)P * d), fitness(P), stash_theta(d), stash_rec(REC_SIZE, 0.0);
+// ---------------------------------------------------------------------------
+// Candidate sharding over several plans (one per device; optimizer.hpp:86-92 allows the
+// population to be evaluated in parallel, :116-121). A generation's P candidates split into
+// contiguous ranges of ceil(P/G); each plan evaluates its range in chunks of its max_batch on
+// its own host thread, and the records come back in slot order. No device-to-device traffic:
+// every plan holds the whole dataset and the winning factor stays on the device that made it.
+namespace {
+
+struct ShardOut {
+  int rc = GPEMU_OK;
+  std::string err;
+  int best_i = -1;  // global candidate index of the shard's best below the threshold
+  double best = INFINITY;
+  std::vector<double> best_rec;
   double jitter_max = 0.0;
-  auto keep_factor = [&](int slot) {
-    if (pl->precision == GPEMU_PRECISION_SINGLE) {
-      ck(cudaMemcpyAsync(pl->factors_f.p + (size_t)stash * pl->slot_stride,
-                         pl->factors_f.p + (size_t)slot * pl->slot_stride,
-                         pl->slot_stride * sizeof(float), cudaMemcpyDeviceToDevice, s),
-         "stash factor");
-      ck(cudaMemcpyAsync(pl->borders_f.p + (size_t)stash * 2 * pl->Npad,
-                         pl->borders_f.p + (size_t)slot * 2 * pl->Npad, 2 * pl->Npad * sizeof(float),
-                         cudaMemcpyDeviceToDevice, s),
-         "stash border");
-    } else {
-      ck(cudaMemcpyAsync(pl->factors.p + (size_t)stash * pl->slot_stride,
-                         pl->factors.p + (size_t)slot * pl->slot_stride,
-                         pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s),
-         "stash factor");
-      ck(cudaMemcpyAsync(pl->borders.p + (size_t)stash * 2 * pl->Npad,
-                         pl->borders.p + (size_t)slot * 2 * pl->Npad, 2 * pl->Npad * sizeof(double),
-                         cudaMemcpyDeviceToDevice, s),
-         "stash border");
-    }
-  };
-  while (ga.gen < ga.G) {
-    // objective lambda (likelihood.hpp:264-273) over the generation: one batch per chunk
-    ga.thetas(thetas.data());
-    const double prev_stash = ga.stash_value;
-    double best = prev_stash;
-    int best_i = -1;
-    for (int c0 = 0; c0 < P; c0 += MB) {
-      const int cn = std::min(MB, P - c0);
-      ck(cudaMemcpyAsync(pl->theta.p, thetas.data() + (size_t)c0 * d, (size_t)cn * d * sizeof(double),
+};
+
+bool same_dataset(const gpemu_plan* a, const gpemu_plan* b) {
+  return a->n == b->n && a->d == b->d && a->p == b->p && a->nugget == b->nugget &&
+         a->precision == b->precision && a->data_hash == b->data_hash;
+}
+
+// Copies a slot's factor + border rows into the plan's stash slot (max_batch).
+void keep_factor(gpemu_plan* pl, int slot) {
+  cudaStream_t s = pl->ctx->stream;
+  const size_t stash = pl->max_batch;
+  if (pl->precision == GPEMU_PRECISION_SINGLE) {
+    ck(cudaMemcpyAsync(pl->factors_f.p + stash * pl->slot_stride, pl->factors_f.p + (size_t)slot * pl->slot_stride,
+                       pl->slot_stride * sizeof(float), cudaMemcpyDeviceToDevice, s), "stash factor");
+    ck(cudaMemcpyAsync(pl->borders_f.p + stash * 2 * pl->Npad, pl->borders_f.p + (size_t)slot * 2 * pl->Npad,
+                       2 * pl->Npad * sizeof(float), cudaMemcpyDeviceToDevice, s), "stash border");
+  } else {
+    ck(cudaMemcpyAsync(pl->factors.p + stash * pl->slot_stride, pl->factors.p + (size_t)slot * pl->slot_stride,
+                       pl->slot_stride * sizeof(double), cudaMemcpyDeviceToDevice, s), "stash factor");
+    ck(cudaMemcpyAsync(pl->borders.p + stash * 2 * pl->Npad, pl->borders.p + (size_t)slot * 2 * pl->Npad,
+                       2 * pl->Npad * sizeof(double), cudaMemcpyDeviceToDevice, s), "stash border");
+  }
+}
+
+// Evaluates candidates [c0, c1) of a generation on one plan, in chunks of max_batch; fitness
+// lands in fitness[c0..c1). With keep, the shard's best candidate strictly below `threshold`
+// (earliest wins ties, likelihood.hpp:267) has its factor saved in the stash slot before a
+// later chunk reuses its slot.
+void eval_shard(gpemu_plan* pl, const double* thetas, int c0, int c1, double threshold, bool keep,
+                double* fitness, double* recs, ShardOut* out) {
+  try {
+    ck(cudaSetDevice(pl->ctx->device), "cudaSetDevice");
+    cudaStream_t s = pl->ctx->stream;
+    const int d = pl->d, MB = (int)pl->max_batch;
+    double best = threshold;
+    for (int a = c0; a < c1; a += MB) {
+      const int cn = std::min(MB, c1 - a);
+      ck(cudaMemcpyAsync(pl->theta.p, thetas + (size_t)a * d, (size_t)cn * d * sizeof(double),
                          cudaMemcpyHostToDevice, s),
          "H2D theta");
-      rc = run_batch(pl, cn);
-      if (rc) return rc;
+      const int rc = run_batch(pl, cn);
+      if (rc) {
+        out->rc = rc;
+        out->err = g_last_error;
+        return;
+      }
       download_records(pl, cn);
       int chunk_best = -1;
       for (int q = 0; q < cn; ++q) {
-        const int i = c0 + q;
+        const int i = a + q;
         const double* r = &pl->h_out[(size_t)q * REC_SIZE];
         fitness[i] = r[REC_NEG2];
-        if (pl->last_ladder[q] >= 0) jitter_max = std::max(jitter_max, kLadder[pl->last_ladder[q]]);
-        if (fitness[i] < best) {  // strict <: the earliest slot wins ties
+        if (recs) std::copy(r, r + REC_SIZE, recs + (size_t)i * REC_SIZE);
+        if (pl->last_ladder[q] >= 0) out->jitter_max = std::max(out->jitter_max, kLadder[pl->last_ladder[q]]);
+        if (fitness[i] < best) {
           best = fitness[i];
-          best_i = i;
+          out->best_i = i;
           chunk_best = q;
         }
       }
-      if (chunk_best >= 0) {  // keep this chunk's winner before the next chunk reuses the slot
+      if (chunk_best >= 0) {
         const double* r = &pl->h_out[(size_t)chunk_best * REC_SIZE];
-        std::copy(r, r + REC_SIZE, stash_rec.begin());
-        std::copy(&thetas[(size_t)best_i * d], &thetas[(size_t)best_i * d] + d, stash_theta.begin());
-        keep_factor(chunk_best);
+        out->best = best;
+        out->best_rec.assign(r, r + REC_SIZE);
+        if (keep) keep_factor(pl, chunk_best);
       }
+    }
+  } catch (const CudaError& e) {
+    out->rc = GPEMU_CUDA;
+    out->err = e.msg;
+  } catch (const std::bad_alloc&) {
+    out->rc = GPEMU_ERROR;
+    out->err = "host allocation failed";
+  }
+}
+
+// Runs eval_shard for every plan (plan k gets range k of ceil(P/G)) on G host threads.
+int eval_sharded(gpemu_plan* const* plans, int G, const double* thetas, int P, double threshold,
+                 bool keep, double* fitness, double* recs, std::vector<ShardOut>& outs) {
+  const int S = (P + G - 1) / G;
+  outs.assign(G, ShardOut{});
+  if (G == 1) {
+    eval_shard(plans[0], thetas, 0, P, threshold, keep, fitness, recs, &outs[0]);
+  } else {
+    std::vector<std::thread> ts;
+    for (int k = 0; k < G; ++k) {
+      const int c0 = std::min(P, k * S), c1 = std::min(P, (k + 1) * S);
+      ts.emplace_back(eval_shard, plans[k], thetas, c0, c1, threshold, keep, fitness, recs, &outs[k]);
+    }
+    for (auto& t : ts) t.join();
+  }
+  for (auto& o : outs)
+    if (o.rc) return set_error(o.rc, "%s", o.err.c_str());
+  return GPEMU_OK;
+}
+
+int check_plans(gpemu_plan* const* plans, int G, const char* who) {
+  if (!plans || G < 1) return set_error(GPEMU_VALIDATION, "%s: need at least one plan", who);
+  for (int k = 0; k < G; ++k) {
+    if (!plans[k]) return set_error(GPEMU_VALIDATION, "%s: null plan %d", who, k);
+    if (!same_dataset(plans[0], plans[k]))
+      return set_error(GPEMU_VALIDATION, "%s: plan %d holds a different dataset / p / nugget / precision", who, k);
+  }
+  return GPEMU_OK;
+}
+
+}  // namespace
+
+int gpemu_eval_batch_multi(gpemu_plan* const* plans, int G, const double* theta, size_t B,
+                           double* neg2, double* mu, double* sigma2, double* jitter,
+                           double* log_det, int* slot_status) {
+  GPEMU_GUARD_BEGIN
+  int rc = check_plans(plans, G, "eval_batch_multi");
+  if (rc) return rc;
+  if (!theta && B) return set_error(GPEMU_VALIDATION, "eval_batch_multi: null theta");
+  if (B == 0) return GPEMU_OK;
+  std::vector<double> fit(B), recs(B * REC_SIZE);
+  std::vector<ShardOut> outs;
+  rc = eval_sharded(plans, G, theta, (int)B, -INFINITY, false, fit.data(), recs.data(), outs);
+  if (rc) return rc;
+  for (size_t b = 0; b < B; ++b) {
+    const double* r = &recs[b * REC_SIZE];
+    if (neg2) neg2[b] = r[REC_NEG2];
+    if (mu) mu[b] = r[REC_MU];
+    if (sigma2) sigma2[b] = r[REC_SIGMA2];
+    if (jitter) jitter[b] = r[REC_JITTER];
+    if (log_det) log_det[b] = r[REC_LOGDET];
+    if (slot_status) slot_status[b] = (int)r[REC_STATUS];
+  }
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_fit_multi(gpemu_plan* const* plans, int G, const double* lo, const double* hi,
+                    const gpemu_ga_config* gac, uint64_t seed, gpemu_fit_result* res,
+                    double* theta_hat, double* alpha, double* trace_best, double* trace_genes,
+                    gpemu_model** model_out) {
+  GPEMU_GUARD_BEGIN
+  int rc = check_plans(plans, G, "fit");
+  if (rc) return rc;
+  if (!lo || !hi || !gac) return set_error(GPEMU_VALIDATION, "fit: null argument");
+  gpemu_ga ga;
+  rc = ga_setup(&ga, plans[0]->d, lo, hi, gac, seed);
+  if (rc) return rc;
+  const int d = plans[0]->d, P = ga.P;
+  std::vector<double> thetas((size_t)P * d), fitness(P), stash_theta(d), stash_rec(REC_SIZE, 0.0);
+  int stash_dev = -1;
+  double jitter_max = 0.0;
+  std::vector<ShardOut> outs;
+  while (ga.gen < ga.G) {
+    nvtx_push("gpemu GA generation");
+    // the objective (likelihood.hpp:264-273) over the generation: one batch per shard chunk
+    ga.thetas(thetas.data());
+    const double prev_stash = ga.stash_value;
+    rc = eval_sharded(plans, G, thetas.data(), P, prev_stash, true, fitness.data(), nullptr, outs);
+    nvtx_pop();
+    if (rc) return rc;
+    int best_i = -1, best_k = -1;
+    double best = prev_stash;
+    for (int k = 0; k < G; ++k) {  // shards in slot order: strict < keeps the earliest slot
+      jitter_max = std::max(jitter_max, outs[k].jitter_max);
+      if (outs[k].best_i >= 0 && outs[k].best < best) {
+        best = outs[k].best;
+        best_i = outs[k].best_i;
+        best_k = k;
+      }
+    }
+    if (best_i >= 0) {
+      stash_dev = best_k;
+      stash_rec = outs[best_k].best_rec;
+      std::copy(&thetas[(size_t)best_i * d], &thetas[(size_t)best_i * d] + d, stash_theta.begin());
     }
     const int gen_now = ga.gen;
     ga.tell(fitness.data());
@@ -1351,14 +1611,16 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
     if (improved != (best_i >= 0) || (improved && ga.stash_slot != best_i))
       return set_error(GPEMU_ERROR, "fit: evaluation stash diverged from the optimizer's");
   }
-  ck(cudaStreamSynchronize(s), "fit");
-  if (!std::isfinite(ga.stash_value))
-    return set_error(GPEMU_FIT, "fit_gp: every candidate failed factorization (n = %d)", pl->n);
+  for (int k = 0; k < G; ++k) ck(cudaStreamSynchronize(plans[k]->ctx->stream), "fit");
+  if (!std::isfinite(ga.stash_value) || stash_dev < 0)
+    return set_error(GPEMU_FIT, "fit_gp: every candidate failed factorization (n = %d)", plans[0]->n);
   if (ga.best_value != ga.stash_value)
     return set_error(GPEMU_ERROR, "fit_gp: optimizer incumbent diverged from evaluation stash");
-  gpemu_model* m = make_model(pl, stash, stash_theta.data(), stash_rec.data());
+  gpemu_plan* owner = plans[stash_dev];  // the model is built where the winning factor lives
+  ck(cudaSetDevice(owner->ctx->device), "cudaSetDevice");
+  gpemu_model* m = make_model(owner, (int)owner->max_batch, stash_theta.data(), stash_rec.data());
   if (theta_hat) std::copy(stash_theta.begin(), stash_theta.end(), theta_hat);
-  if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+  if (alpha) d2h_sync(alpha, m->alpha.p, owner->n * sizeof(double), m->ctx->stream, "D2H alpha");
   if (trace_best) std::copy(ga.trace_best.begin(), ga.trace_best.end(), trace_best);
   if (trace_genes) std::copy(ga.trace_genes.begin(), ga.trace_genes.end(), trace_genes);
   if (res) {
@@ -1366,17 +1628,28 @@ int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga
     res->mu_hat = stash_rec[REC_MU];
     res->sigma2_hat = stash_rec[REC_SIGMA2];
     res->jitter_max = jitter_max;
-    res->r_builds = pl->r_builds;
-    res->factorizations = pl->factorizations;
-    res->triangular_solves = pl->solves;
+    res->r_builds = res->factorizations = res->triangular_solves = 0;
+    for (int k = 0; k < G; ++k) {
+      res->r_builds += plans[k]->r_builds;
+      res->factorizations += plans[k]->factorizations;
+      res->triangular_solves += plans[k]->solves;
+    }
   }
   if (model_out) {
     *model_out = m;
   } else {
-    delete m;
+    release(m);
   }
   return GPEMU_OK;
   GPEMU_GUARD_END
+}
+
+int gpemu_fit(gpemu_plan* pl, const double* lo, const double* hi, const gpemu_ga_config* gac,
+              uint64_t seed, gpemu_fit_result* res, double* theta_hat, double* alpha,
+              double* trace_best, double* trace_genes, gpemu_model** model_out) {
+  if (!pl) return set_error(GPEMU_VALIDATION, "fit: null argument");
+  return gpemu_fit_multi(&pl, 1, lo, hi, gac, seed, res, theta_hat, alpha, trace_best, trace_genes,
+                         model_out);
 }
 
 // bench.hpp:302-383 detail::refine_fit: coordinate-wise golden-section polish, `budget`
@@ -1397,6 +1670,7 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
                         double* neg2_out, int* evals_out, gpemu_model** model_out, double* scalars,
                         double* alpha) {
   GPEMU_GUARD_BEGIN
+  NvtxRange range("refine_fit polish");
   if (!rebuild) rebuild = pl;
   if (!pl || pl->d != rebuild->d || pl->n != rebuild->n)
     return set_error(GPEMU_VALIDATION, "refine_fit: polish and rebuild plans must share the dataset");
@@ -1434,6 +1708,21 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
   // that count). Needs 8 slots; smaller plans evaluate one candidate at a time.
   const bool spec = pl->max_batch >= 8;
   const uint64_t led_r = pl->r_builds, led_f = pl->factorizations, led_s = pl->solves;
+  // the ledger counts the polish's evaluations, not the speculative extras, on every exit path
+  struct LedgerRestore {
+    gpemu_plan* pl;
+    bool on;
+    uint64_t r, f, s;
+    const int* used;
+    void apply() {
+      if (!on) return;
+      on = false;
+      pl->r_builds = r + *used;
+      pl->factorizations = f + *used;
+      pl->solves = s + 2 * (uint64_t)*used;
+    }
+    ~LedgerRestore() { apply(); }
+  } led_restore{pl, spec, led_r, led_f, led_s, &used};
   double sp_x[8], sp_v[8];
   int sp_n = 0, sp_k = -1;
   auto speculate = [&](int k, double a, double b, double x1, double x2) {
@@ -1464,14 +1753,18 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
       for (int q = 0; q < d; ++q) th[(size_t)i * d + q] = std::pow(10.0, q == k ? pts[i] : best[q]);
     ck(cudaMemcpyAsync(pl->theta.p, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice, s),
        "H2D theta");
-    rc = run_batch(pl, 8);
+    rc = run_batch(pl, 8, /*tolerate_nonfinite=*/true);
     if (rc) return;
     download_records(pl, 8);
+    sp_n = 0;
     for (int i = 0; i < 8; ++i) {
-      sp_x[i] = pts[i];
-      sp_v[i] = pl->h_out[(size_t)i * REC_SIZE + REC_NEG2];
+      // a non-finite point is left out: if the replay visits it, it is evaluated on its own
+      // and fails as the sequential polish does
+      if (pl->h_out[(size_t)i * REC_SIZE + REC_STATUS] == 2.0) continue;
+      sp_x[sp_n] = pts[i];
+      sp_v[sp_n] = pl->h_out[(size_t)i * REC_SIZE + REC_NEG2];
+      ++sp_n;
     }
-    sp_n = 8;
     sp_k = k;
   };
   auto eval_genes = [&](const std::vector<double>& genes, int k) -> double {
@@ -1531,11 +1824,7 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
     }
     k = (k + 1) % d;
   }
-  if (spec) {  // the ledger counts the polish's evaluations, not the speculative extras
-    pl->r_builds = led_r + used;
-    pl->factorizations = led_f + used;
-    pl->solves = led_s + 2 * (uint64_t)used;
-  }
+  led_restore.apply();  // before the model rebuild adds its own evaluation
   for (int q = 0; q < d; ++q) theta[q] = std::pow(10.0, best[q]);
   if (theta_out) std::copy(theta.begin(), theta.end(), theta_out);
   if (neg2_out) *neg2_out = best_value;
@@ -1557,7 +1846,7 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
           scalars[2] = m->sigma2;
           scalars[3] = m->jitter;
         }
-        if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+        if (alpha) d2h_sync(alpha, m->alpha.p, pl->n * sizeof(double), m->ctx->stream, "D2H alpha");
         *model_out = m;
       }
     }
@@ -1585,11 +1874,11 @@ int gpemu_model_at_theta(gpemu_plan* pl, const double* theta, gpemu_model** mode
     scalars[2] = m->sigma2;
     scalars[3] = m->jitter;
   }
-  if (alpha) ck(cudaMemcpy(alpha, m->alpha.p, pl->n * sizeof(double), cudaMemcpyDeviceToHost), "D2H alpha");
+  if (alpha) d2h_sync(alpha, m->alpha.p, pl->n * sizeof(double), m->ctx->stream, "D2H alpha");
   if (model_out) {
     *model_out = m;
   } else {
-    delete m;
+    release(m);
   }
   return GPEMU_OK;
   GPEMU_GUARD_END
@@ -1605,12 +1894,13 @@ int gpemu_model_scalars(const gpemu_model* m, double* out) {
 }
 
 int gpemu_model_destroy(gpemu_model* m) {
-  delete m;
+  release(m);
   return GPEMU_OK;
 }
 
 int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, double* mse) {
   GPEMU_GUARD_BEGIN
+  NvtxRange range(mse ? "K4 predict + kriging MSE" : "K4 predict");
   if (!m || (!Xtest && N) || (!yhat && N)) return set_error(GPEMU_VALIDATION, "predict: null argument");
   int rc = validate_unit_cube(Xtest, N, m->d, "predict");
   if (rc) return set_error(GPEMU_VALIDATION, "predict: test point outside the unit cube");
@@ -1648,12 +1938,12 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
     if (m->ext_rt_cap < rt_cap) {
       m->ext.alloc((size_t)rt_cap * NT * TILE_ELEMS);
       m->ext_flags.alloc((size_t)rt_cap * NT);
-      ck(cudaMemset(m->ext_flags.p, 0, (size_t)rt_cap * NT * sizeof(int)), "memset");
+      ck(cudaMemsetAsync(m->ext_flags.p, 0, (size_t)rt_cap * NT * sizeof(int), s), "memset");
       m->ext_slot.alloc(1);
-      ck(cudaMemset(m->ext_slot.p, 0, sizeof(int)), "memset");
+      ck(cudaMemsetAsync(m->ext_slot.p, 0, sizeof(int), s), "memset");
       m->counter.alloc(1);
       m->error.alloc(1);
-      ck(cudaMemset(m->error.p, 0, sizeof(int)), "memset");
+      ck(cudaMemsetAsync(m->error.p, 0, sizeof(int), s), "memset");
       m->ext_rt_cap = rt_cap;
     }
     for (size_t p0 = 0; p0 < N; p0 += chunk_pts) {
@@ -1696,7 +1986,7 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   ck(cudaStreamSynchronize(s), "predict");
   if (mse && m->error.p) {
     int err = 0;
-    ck(cudaMemcpy(&err, m->error.p, sizeof(int), cudaMemcpyDeviceToHost), "D2H error");
+    d2h_sync(&err, m->error.p, sizeof(int), m->ctx->stream, "D2H error");
     if (err) return set_error(GPEMU_CUDA, "chol_dag (extension): dependency wait timed out");
   }
   if (hbad) return set_error(GPEMU_NONFINITE, "corr_vector: non-finite correlation value");

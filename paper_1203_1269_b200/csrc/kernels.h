@@ -18,7 +18,7 @@ void launch_pow_table(const double* X, int n, int d, double p, int NT, double* t
 void launch_assemble(const double* table, const double* theta /*[slot][d]*/, const double* y,
                      int n, int d, double nugget, int NT, const int* slots, int nslots,
                      const double* jitter, double* factors, size_t slot_stride, double* borders,
-                     int* status, cudaStream_t s);
+                     int* status, int num_sms, cudaStream_t s);
 // Row-major n x n R for one theta (build_corr_matrix, correlation.hpp:99-146).
 void launch_build_corr_rowmajor(const double* X, int n, int d, const double* theta, double p,
                                 double nugget, double* R, int* bad, cudaStream_t s);
@@ -69,10 +69,15 @@ void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, dou
                               cudaStream_t s);
 // Tiled -> row-major lower with strict upper zeroed.
 void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s);
-// Forward (upper=0: L x = b) or backward (upper=1: L^T x = b) substitution on a
-// tiled factor (backend.hpp:129-153). One CTA.
-void launch_tri_solve(const double* tiles, int n, int NT, const double* b, double* x, int upper,
-                      cudaStream_t s);
+// Blocked triangular solve on a tiled factor (kernels_trsv.cu, backend.hpp:129-153): forward
+// (upper=0: L x = b) or backward (upper=1: L^T x = b). Right-hand side b[i] - mu * b2[i]
+// (b2 nullable) for i < nb, zero past it; x: NT * 128 doubles (also the inter-block exchange).
+// flags: NT ints never equal to a fresh `epoch` (epoch-valued, not cleared); counter: 1 int
+// (reset by the launcher); error: deadlock-guard word.
+void launch_tile_trsv(const double* tiles, int NT, const double* b, const double* b2, double mu,
+                      int nb, double* x, int upper, int* flags, int* counter, int epoch,
+                      int* error, int num_sms, cudaStream_t s);
+size_t tile_trsv_smem_bytes();
 
 // ---- K4: prediction (kernels_predict.cu) -----------------------------------
 // yhat_j = mu + r_j' alpha for N test points (predictor.hpp:20-50), in a fixed summation

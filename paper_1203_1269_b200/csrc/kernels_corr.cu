@@ -157,14 +157,14 @@ static void launch_asm(dim3 grid, cudaStream_t s, const double* table, const dou
 void launch_assemble(const double* table, const double* theta, const double* y, int n, int d,
                      double nugget, int NT, const int* slots, int nslots, const double* jitter,
                      double* factors, size_t slot_stride, double* borders, int* status,
-                     cudaStream_t s) {
+                     int num_sms, cudaStream_t s) {
   const int Npad = NT * TILE;
   border_init_kernel<<<dim3((Npad + 255) / 256 < 32 ? (Npad + 255) / 256 : 32, nslots), 256, 0, s>>>(
       y, n, Npad, slots, borders, status);
   // at least ~8 blocks per SM on small designs (n=200 has 3 tiles: 24 blocks with a fixed 8),
   // at most one element per thread per slot chunk (TILE_ELEMS / 256 = 64)
   const int tiles = num_tiles(NT);
-  const int gy = std::min(64, std::max(8, (1184 + tiles - 1) / tiles));
+  const int gy = std::min(64, std::max(8, (8 * num_sms + tiles - 1) / tiles));
   const dim3 grid(tiles, gy);
   // theta entries beyond d are zero in shared memory, so a looser bound is only slower
 #define GPEMU_ASM(D) \

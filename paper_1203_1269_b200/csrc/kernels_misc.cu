@@ -1,11 +1,10 @@
-// kernels_misc.cu -- K3 deviance finalisation, layout conversion, single-RHS solves.
+// kernels_misc.cu -- K3 deviance finalisation, layout conversion.
 //
 // Reference (relative to /root/reference/proj/include/gpemu/):
 //   factorize_into log-det    backend.hpp:111-113   2 * sum_i log L_ii, sequential, double
 //   dot_accumulate            matrix.hpp:64-69      sequential double dot
 //   eval tail                 likelihood.hpp:124-140
 //   sigma2_hat_from_parts     likelihood.hpp:63-66
-//   solve_lower/upper_into    backend.hpp:129-153
 // The scalar tail keeps the reference's sequential summation order (one thread
 // per sum, the four sums concurrent, operands staged in shared memory) and rounds
 // every product/sum separately.
@@ -147,47 +146,6 @@ __global__ void tiles_to_rowmajor_kernel(const double* __restrict__ tiles, int n
 
 void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s) {
   tiles_to_rowmajor_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(tiles, n, L);
-}
-
-// Column-oriented substitution; per entry the subtraction order matches the
-// reference's row-oriented loop for the forward solve (ascending k).
-__global__ void __launch_bounds__(1024) tri_solve_kernel(const double* __restrict__ tiles, int n,
-                                                         const double* __restrict__ b,
-                                                         double* __restrict__ x, int upper) {
-  extern __shared__ double w[];
-  for (int i = threadIdx.x; i < n; i += blockDim.x) w[i] = b[i];
-  __syncthreads();
-  auto Lat = [&](int i, int j) {
-    return tiles[tile_index(i >> 7, j >> 7) * TILE_ELEMS + elem_off(i & 127, j & 127)];
-  };
-  if (!upper) {
-    for (int k = 0; k < n; ++k) {
-      const double xk = w[k] / Lat(k, k);
-      __syncthreads();
-      for (int l = k + 1 + threadIdx.x; l < n; l += blockDim.x)
-        w[l] = __dsub_rn(w[l], __dmul_rn(Lat(l, k), xk));
-      if (threadIdx.x == 0) w[k] = xk;
-      __syncthreads();
-    }
-  } else {
-    for (int k = n - 1; k >= 0; --k) {
-      const double xk = w[k] / Lat(k, k);
-      __syncthreads();
-      for (int l = threadIdx.x; l < k; l += blockDim.x)
-        w[l] = __dsub_rn(w[l], __dmul_rn(Lat(k, l), xk));
-      if (threadIdx.x == 0) w[k] = xk;
-      __syncthreads();
-    }
-  }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = w[i];
-}
-
-void launch_tri_solve(const double* tiles, int n, int NT, const double* b, double* x, int upper,
-                      cudaStream_t s) {
-  const size_t smem = (size_t)n * sizeof(double);
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(tri_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  tri_solve_kernel<<<1, 1024, smem, s>>>(tiles, n, b, x, upper);
 }
 
 }  // namespace gpemu_dev

@@ -76,7 +76,8 @@ EXPORTED_SYMBOLS = (
     "gpemu_plan_dag_profile", "gpemu_try_cholesky", "gpemu_ga_create", "gpemu_ga_destroy",
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
     "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
-    "gpemu_ctx_mem_info", "gpemu_plan_bytes", "gpemu_ticket_order",
+    "gpemu_ctx_mem_info", "gpemu_plan_bytes", "gpemu_ticket_order", "gpemu_ctx_num_sms",
+    "gpemu_eval_batch_multi", "gpemu_fit_multi",
 )
 
 
@@ -112,6 +113,7 @@ def lib():
     L.gpemu_ctx_set_engine.argtypes = [_vp, C.c_int]
     L.gpemu_ctx_launch_count.argtypes = [_vp]
     L.gpemu_ctx_launch_count.restype = C.c_uint64
+    L.gpemu_ctx_num_sms.argtypes = [_vp]
     L.gpemu_build_corr.argtypes = [_vp, _dp, _sz, _sz, _dp, C.c_double, C.c_double, _dp]
     L.gpemu_corr_vector.argtypes = [_vp, _dp, _dp, _sz, _sz, _dp, C.c_double, _dp]
     L.gpemu_factorize.argtypes = [_vp, _dp, _sz, _dp, _dp, _dp]
@@ -140,6 +142,11 @@ def lib():
     L.gpemu_ticket_order.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, _sz]
     L.gpemu_fit.argtypes = [_vp, _dp, _dp, C.POINTER(_GaConfigC), C.c_uint64,
                             C.POINTER(_FitResultC), _dp, _dp, _dp, _dp, C.POINTER(_vp)]
+    L.gpemu_fit_multi.argtypes = [C.POINTER(_vp), C.c_int, _dp, _dp, C.POINTER(_GaConfigC),
+                                  C.c_uint64, C.POINTER(_FitResultC), _dp, _dp, _dp, _dp,
+                                  C.POINTER(_vp)]
+    L.gpemu_eval_batch_multi.argtypes = [C.POINTER(_vp), C.c_int, _dp, _sz, _dp, _dp, _dp, _dp,
+                                         _dp, _ip]
     L.gpemu_model_at_theta.argtypes = [_vp, _dp, C.POINTER(_vp), _dp, _dp]
     L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
@@ -190,6 +197,10 @@ class Context:
     @property
     def launch_count(self) -> int:
         return int(lib().gpemu_ctx_launch_count(self.handle))
+
+    @property
+    def num_sms(self) -> int:
+        return int(lib().gpemu_ctx_num_sms(self.handle))
 
     def close(self):
         if getattr(self, "handle", None):
@@ -603,14 +614,15 @@ class ProfileEvaluator:
 
     def dag_profile(self, enable: bool = True, read: bool = False):
         """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""
-        out = np.zeros(148 * 24 + 256 + 65536 * 4, dtype=np.uint64) if read else None
+        sms = self.backend.ctx.num_sms  # the C side lays the counters out per CTA (one per SM)
+        out = np.zeros(sms * 24 + 256 + 65536 * 4, dtype=np.uint64) if read else None
         _check(lib().gpemu_plan_dag_profile(self.handle, int(enable),
                                             None if out is None else out.ctypes.data, 0 if out is None else out.size))
         if out is None:
             return None
-        m = out[:148 * 24].reshape(-1, 24)
+        m = out[:sms * 24].reshape(-1, 24)
         res = {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
-        res["trace"] = out[148 * 24 + 256:].reshape(-1, 4)  # per ticket: start, gemm end, publish, end (ns)
+        res["trace"] = out[sms * 24 + 256:].reshape(-1, 4)  # per ticket: start, gemm end, publish, end (ns)
         return res
 
     def eval_batch_device(self, theta_ptr: int, B: int, out_ptr: int):
@@ -667,13 +679,9 @@ class ProfileEvaluator:
 
 
 def neg2_log_profile(theta, data: Dataset, cfg: FitConfig, backend: Backend) -> ProfileEval:
-    """likelihood.hpp:161-166."""
-    # 8 slots let the polish evaluate each coordinate's golden-section decision tree in one
-    # batch (same theta / -2logL / count as one-at-a-time, see gpemu_refine_fit_ex)
-    free, tot = C.c_size_t(), C.c_size_t()
-    _check(lib().gpemu_ctx_mem_info(backend.ctx.handle, C.byref(free), C.byref(tot)))
-    mb = 8 if lib().gpemu_plan_bytes(data.n(), d, 8, 0) <= 0.9 * free.value else 1
-    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=mb)
+    """likelihood.hpp:161-166: one evaluation, so a one-slot plan."""
+    ev = ProfileEvaluator(data, cfg.p, cfg.nugget, backend, max_batch=1,
+                          precision=cfg.precision)
     try:
         return ev.eval(theta)
     finally:
@@ -800,13 +808,17 @@ def fit_batch(data: Dataset, cfg: FitConfig, backend: Backend, reserve: float = 
 
 def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
                     evaluator: Optional[ProfileEvaluator] = None) -> FitResult:
-    """likelihood.hpp:243-303: one device batch per GA generation."""
+    """likelihood.hpp:243-303: one device batch per GA generation. `evaluator` may be a list
+    of ProfileEvaluators of the same data on several devices: each generation is then split
+    into contiguous candidate ranges, one per evaluator, run concurrently (gpemu_fit_multi);
+    theta-hat and the trace are bitwise the one-device fit's."""
     d = data.d()
     bounds = cfg.bounds_for(d)
     own = evaluator is None
     ev = evaluator or ProfileEvaluator(data, cfg.p, cfg.nugget, backend,
                                        max_batch=fit_batch(data, cfg, backend),
                                        precision=cfg.precision)
+    evs = list(ev) if isinstance(ev, (list, tuple)) else [ev]
     try:
         lo = _f64([b[0] for b in bounds])
         hi = _f64([b[1] for b in bounds])
@@ -818,8 +830,10 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
         tb = np.empty(cfg.ga.generations)
         tg = np.empty((cfg.ga.generations, d))
         mh = _vp()
-        _check(lib().gpemu_fit(ev.handle, _p(lo), _p(hi), C.byref(ga), C.c_uint64(cfg.seed),
-                               C.byref(res), _p(theta), _p(alpha), _p(tb), _p(tg), C.byref(mh)))
+        hs = (_vp * len(evs))(*[e.handle for e in evs])
+        _check(lib().gpemu_fit_multi(hs, len(evs), _p(lo), _p(hi), C.byref(ga),
+                                     C.c_uint64(cfg.seed), C.byref(res), _p(theta), _p(alpha),
+                                     _p(tb), _p(tg), C.byref(mh)))
         led = backend.ledger()
         B = cfg.ga.budget()
         led.add_r_build(B)
@@ -827,6 +841,7 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
         led.add_triangular_solves(2 * B + 2)
         model = GpModel(mh, data, Hyperparameters(list(theta), cfg.p, cfg.nugget), res.mu_hat,
                         res.sigma2_hat, res.neg2_log_lik, alpha, backend.ctx)
+        model._contexts = [e.backend.ctx for e in evs]  # the model lives on one of them
         trace = GaTrace([GaGenerationRecord(float(tb[g]), list(tg[g]),
                                             (g + 1) * cfg.ga.population)
                          for g in range(cfg.ga.generations)])
@@ -834,6 +849,22 @@ def fit_gp_detailed(data: Dataset, cfg: FitConfig, backend: Backend,
     finally:
         if own:
             ev.close()
+
+
+def eval_batch_multi(evaluators: Sequence[ProfileEvaluator], thetas) -> dict:
+    """B independent evaluations sharded over several evaluators of the same data (one per
+    device; contiguous ranges of ceil(B/G), concurrent host threads, gpemu_eval_batch_multi).
+    Records come back in slot order, bitwise those of one evaluator."""
+    T = _f64(np.atleast_2d(thetas))
+    B = T.shape[0]
+    out = {k: np.empty(B) for k in ("neg2", "mu", "sigma2", "jitter", "log_det")}
+    st = np.empty(B, dtype=np.int32)
+    hs = (_vp * len(evaluators))(*[e.handle for e in evaluators])
+    _check(lib().gpemu_eval_batch_multi(hs, len(evaluators), _p(T), B, _p(out["neg2"]),
+                                        _p(out["mu"]), _p(out["sigma2"]), _p(out["jitter"]),
+                                        _p(out["log_det"]), st.ctypes.data_as(_ip)))
+    out["status"] = st
+    return out
 
 
 def refine_fit(fit: FitResult, data: Dataset, cfg: FitConfig, backend: Backend,

@@ -160,8 +160,10 @@ def test_eval_batch_c1_goldens(g, name, engine):
 
 
 def test_eval_batch_c2_golden(g, ctx):
+    """Config C2: the full 64-candidate batch (n=2048, d=6, p=1.95) in one device batch."""
     z = np.load(os.path.join(GOLD, "c2.npz"))
-    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), 1.95, 0.0, g.Backend(ctx), max_batch=16)
+    assert z["thetas"].shape == (64, 6)
+    ev = g.ProfileEvaluator(g.new_dataset(z["X"], z["y"]), 1.95, 0.0, g.Backend(ctx), max_batch=64)
     r = ev.eval_batch(z["thetas"])
     assert np.array_equal(r["jitter"], z["jitter"])
     gate_neg2(r["neg2"], z)

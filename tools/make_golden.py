@@ -7,7 +7,8 @@ time only); the fixtures are committed and travel to the GPU box.
   c1.npz    config C1 (n=200, d=2, p=2, goldstein_price_log): 100 GA-style thetas, the fit
             (GA 100x20) and 1000 test-point predictions
   c1p195.npz  same design, p=1.95 (self-discrepancy stress: near-singular thetas)
-  c2.npz    config C2 design (n=2048, d=6, p=1.95, hartman6) with 16 thetas
+  c2.npz    config C2 design (n=2048, d=6, p=1.95, hartman6) with 16 thetas (the committed
+            fixture holds all 64: tools/make_golden_c2_full.py)
 Each eval set also stores `self_disc` (the reference's native build: ReferenceBackend vs
 ParallelBackend), `truth` (long-double deviance of the same double R) and `sens` (max relative
 change of that long-double deviance under random 1-ulp perturbations of R: the conditioning
