@@ -236,6 +236,19 @@ GPEMU_API int gpemu_model_at_theta(gpemu_plan* plan, const double* theta, gpemu_
 /* A model's scalars: out[4] = {neg2_log_lik, mu_hat, sigma2_hat, jitter_used}
  * (GpModel fields, likelihood.hpp:171-182; factor.jitter_used, backend.hpp:54-70). */
 GPEMU_API int gpemu_model_scalars(const gpemu_model* model, double* out);
+/* A model's factor (CorrelationFactor::lower, backend.hpp:54-70): L_out n x n row-major with the
+ * strict upper zeroed (nullable: log_det only), log_det = log|R + jitter I|. */
+GPEMU_API int gpemu_model_factor(gpemu_model* model, double* L_out, double* log_det);
+/* A model's alpha = (R + jitter I)^-1 (y - mu 1) (GpModel::alpha, n doubles). */
+GPEMU_API int gpemu_model_alpha(gpemu_model* model, double* alpha_out);
+/* A device model from a GpModel assembled elsewhere (likelihood.hpp:171-182: the training inputs
+ * X n x d, params theta / p, scalars[4] = {neg2_log_lik, mu_hat, sigma2_hat, jitter_used},
+ * factor.log_det, factor.lower L n x n row-major (lower triangle read), alpha n). v = L^-1 1 for
+ * the MSE is solved on the device. Lets predict() take any reference GpModel<double>. */
+GPEMU_API int gpemu_model_import(gpemu_ctx* ctx, const double* X, size_t n, size_t d,
+                                 const double* theta, double p, const double* scalars,
+                                 double log_det, const double* L, const double* alpha,
+                                 gpemu_model** out);
 GPEMU_API int gpemu_model_destroy(gpemu_model* model);
 
 /* ---- predictor.hpp ------------------------------------------------------ */

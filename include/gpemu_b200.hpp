@@ -244,6 +244,7 @@ class AcceleratedBackend final : public gpemu::Backend<double> {
   explicit AcceleratedBackend(int device = 0) : ctx_(std::make_shared<Context>(device)) {}
   gpemu::BackendKind kind() const override { return gpemu::BackendKind::kAccelerated; }
   std::string_view name() const override { return "accelerated"; }
+  Context& context() { return *ctx_; }
 
  protected:
   // In place on the lower triangle; false when a pivot is not strictly positive (or NaN).
@@ -263,6 +264,305 @@ inline void register_accelerated(int device = 0) {
   gpemu::register_backend<double>("accelerated", [device](unsigned) {
     return std::make_unique<AcceleratedBackend>(device);
   });
+}
+
+// ---------------------------------------------------------------------------------------
+// 3. Same-signature fast path. The reference's entry points with the reference's argument
+//    types -- ProfileEvaluator(const Dataset&, p, nugget, Backend&) (likelihood.hpp:77),
+//    neg2_log_profile (:161-166), model_at_theta (:216-237), fit_gp_detailed / fit_gp
+//    (:243-308), predict / predict_set (predictor.hpp:20-79) -- taking an AcceleratedBackend
+//    and running the BATCHED device path (a GA generation is one device batch, prediction is
+//    one kernel over all test points), not the per-attempt try_cholesky hook. Switching a
+//    reference program is a namespace change: `gpemu::fit_gp_detailed(data, cfg, backend)`
+//    -> `gpemu_b200::fit_gp_detailed(data, cfg, accelerated_backend)`; the results carry the
+//    reference's types (gpemu::ProfileEval, gpemu::GpModel<double>, gpemu::GaTrace) and the
+//    backend's Ledger counts what the reference's would.
+
+// GpModel<double> (likelihood.hpp:171-182) plus the device-resident model it was built from.
+// Slicing to gpemu::GpModel<double> keeps every reference field; predict() on a plain
+// GpModel<double> re-imports it to the device (gpemu_model_import).
+struct DeviceGpModel : gpemu::GpModel<double> {
+  std::shared_ptr<Model> device;
+};
+
+// FitResult<double> (likelihood.hpp:185-190) with a DeviceGpModel; converts to the reference type.
+struct DeviceFitResult {
+  DeviceGpModel model;
+  gpemu::GaTrace trace;
+  double jitter_max = 0.0;
+  operator gpemu::FitResult<double>() const { return {model, trace, jitter_max}; }
+};
+
+namespace detail {
+
+inline std::vector<double> row_major(const gpemu::Matrix<double>& m) {
+  return std::vector<double>(m.data(), m.data() + m.rows() * m.cols());
+}
+
+// A reference GpModel around a device model: scalars, alpha and the factor come back from the
+// device (the factor as the dense lower triangle the reference keeps).
+inline DeviceGpModel wrap_model(gpemu_model* h, const gpemu::Dataset& data, std::vector<double> theta,
+                                double p, double nugget, bool with_factor = true) {
+  DeviceGpModel m;
+  m.device = std::make_shared<Model>(h);
+  double sc[4];
+  check(gpemu_model_scalars(h, sc));
+  const std::size_t n = data.n();
+  m.dataset = data;
+  m.params = gpemu::Hyperparameters{std::move(theta), p, nugget};
+  m.neg2_log_lik = sc[0];
+  m.mu_hat = sc[1];
+  m.sigma2_hat = sc[2];
+  m.factor.jitter_used = sc[3];
+  if (with_factor) {
+    m.factor.lower = gpemu::Matrix<double>(n, n);
+    check(gpemu_model_factor(h, m.factor.lower.data(), &m.factor.log_det));
+  } else {
+    check(gpemu_model_factor(h, nullptr, &m.factor.log_det));
+  }
+  m.inputs_scalar = data.inputs();
+  return m;
+}
+
+inline gpemu_ga_config ga_config(const gpemu::GaConfig& g) {
+  return gpemu_ga_config{g.population, g.generations, g.crossover_rate, g.mutation_sigma,
+                         g.mutation_prob, g.elitism};
+}
+
+// Candidate slots for a fit plan: the whole population when it fits in 90% of free device
+// memory, else as many as fit (the generation is then evaluated in chunks, same theta-hat).
+inline std::size_t fit_slots(gpemu_ctx* ctx, const gpemu::Dataset& data, int population) {
+  std::size_t free_b = 0, total_b = 0;
+  check(gpemu_ctx_mem_info(ctx, &free_b, &total_b));
+  const double budget = 0.9 * static_cast<double>(free_b);
+  std::size_t lo = 1, hi = static_cast<std::size_t>(population);
+  if (static_cast<double>(gpemu_plan_bytes(data.n(), data.d(), hi, GPEMU_PRECISION_DOUBLE)) <= budget) return hi;
+  while (lo < hi) {
+    const std::size_t mid = (lo + hi + 1) / 2;
+    if (static_cast<double>(gpemu_plan_bytes(data.n(), data.d(), mid, GPEMU_PRECISION_DOUBLE)) <= budget)
+      lo = mid;
+    else
+      hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace detail
+
+// ProfileEvaluator (likelihood.hpp:74-158) with the reference's constructor signature; eval()
+// is one device evaluation, eval_batch() evaluates B thetas (B x d row-major) in one batch.
+class ProfileEvaluator {
+ public:
+  ProfileEvaluator(const gpemu::Dataset& data, double p, double nugget, AcceleratedBackend& backend,
+                   std::size_t max_batch = 128)
+      : backend_(backend), n_(data.n()), d_(data.d()), inputs_(data.inputs()), y_(data.outputs()) {
+    gpemu::Hyperparameters probe{std::vector<double>(d_, 1.0), p, nugget};
+    probe.validate(d_);
+    check(gpemu_plan_create(backend.context().get(), inputs_.data(), y_.data(), n_, d_, p, nugget,
+                            max_batch, &h_));
+    max_batch_ = max_batch;
+  }
+  ~ProfileEvaluator() { gpemu_plan_destroy(h_); }
+  ProfileEvaluator(const ProfileEvaluator&) = delete;
+  ProfileEvaluator& operator=(const ProfileEvaluator&) = delete;
+
+  std::size_t n() const { return n_; }
+  std::size_t d() const { return d_; }
+  const std::vector<double>& outputs() const { return y_; }
+  const gpemu::Matrix<double>& inputs() const { return inputs_; }
+  double jitter_max() const { return jitter_max_; }
+  gpemu_plan* get() const { return h_; }
+
+  std::vector<gpemu::ProfileEval> eval_batch(std::span<const double> thetas) {
+    const std::size_t B = thetas.size() / d_;
+    std::vector<gpemu::ProfileEval> out(B);
+    std::vector<double> neg2(B), mu(B), s2(B), jit(B);
+    std::vector<int> st(B);
+    for (std::size_t b0 = 0; b0 < B; b0 += max_batch_) {
+      const std::size_t cb = std::min(max_batch_, B - b0);
+      check(gpemu_eval_batch(h_, thetas.data() + b0 * d_, cb, neg2.data() + b0, mu.data() + b0,
+                             s2.data() + b0, jit.data() + b0, nullptr, st.data() + b0));
+      last_b0_ = b0;
+    }
+    for (std::size_t b = 0; b < B; ++b) {
+      out[b].theta.assign(thetas.begin() + b * d_, thetas.begin() + (b + 1) * d_);
+      auto& ledger = backend_.ledger();  // each eval: one R build, one factorization, two solves
+      ledger.add_r_build();
+      ledger.add_factorization();
+      if (st[b] == GPEMU_SLOT_NOT_PD) continue;  // +inf (likelihood.hpp:115-119)
+      ledger.add_triangular_solves(2);
+      jitter_max_ = std::max(jitter_max_, jit[b]);
+      if (st[b] != GPEMU_SLOT_OK) continue;  // degenerate vtv: +inf, zero fields
+      out[b].neg2_log_lik = neg2[b];
+      out[b].mu_hat = mu[b];
+      out[b].sigma2_hat = s2[b];
+      out[b].jitter_used = jit[b];
+    }
+    last_slot_ = B ? static_cast<long>(B - 1 - last_b0_) : -1;
+    factor_valid_ = false;
+    return out;
+  }
+  gpemu::ProfileEval eval(std::span<const double> theta) { return eval_batch(theta).front(); }
+
+  // The factor of the most recent evaluation (the last theta of the last eval_batch),
+  // downloaded on first use.
+  const gpemu::CorrelationFactor<double>& last_factor() {
+    if (!factor_valid_) {
+      if (last_slot_ < 0) throw gpemu::Error("last_factor: no evaluation yet");
+      factor_.lower = gpemu::Matrix<double>(n_, n_);
+      check(gpemu_plan_last_factor(h_, static_cast<std::size_t>(last_slot_), factor_.lower.data(),
+                                   &factor_.log_det, &factor_.jitter_used));
+      factor_valid_ = true;
+    }
+    return factor_;
+  }
+
+ private:
+  AcceleratedBackend& backend_;
+  std::size_t n_, d_, max_batch_ = 1, last_b0_ = 0;
+  gpemu::Matrix<double> inputs_;
+  std::vector<double> y_;
+  gpemu_plan* h_ = nullptr;
+  double jitter_max_ = 0.0;
+  long last_slot_ = -1;
+  bool factor_valid_ = false;
+  gpemu::CorrelationFactor<double> factor_;
+};
+
+// neg2_log_profile (likelihood.hpp:161-166).
+inline gpemu::ProfileEval neg2_log_profile(std::span<const double> theta, const gpemu::Dataset& data,
+                                           const gpemu::FitConfig& cfg, AcceleratedBackend& backend) {
+  ProfileEvaluator ev(data, cfg.p, cfg.nugget, backend, 1);
+  return ev.eval(theta);
+}
+
+// model_at_theta (likelihood.hpp:216-237): one evaluation plus alpha, on the device.
+inline DeviceGpModel model_at_theta(const gpemu::Dataset& data, std::span<const double> theta,
+                                    double p, double nugget, AcceleratedBackend& backend) {
+  ProfileEvaluator ev(data, p, nugget, backend, 1);
+  gpemu_model* h = nullptr;
+  const int rc = gpemu_model_at_theta(ev.get(), theta.data(), &h, nullptr, nullptr);
+  auto& ledger = backend.ledger();
+  ledger.add_r_build();
+  ledger.add_factorization();
+  check(rc);  // NotPositiveDefiniteError when every ladder step failed
+  ledger.add_triangular_solves(4);  // the evaluation's two + solve_full's two
+  DeviceGpModel m = detail::wrap_model(h, data, std::vector<double>(theta.begin(), theta.end()), p, nugget);
+  m.alpha.resize(data.n());
+  check(gpemu_model_alpha(h, m.alpha.data()));
+  return m;
+}
+
+// fit_gp_detailed (likelihood.hpp:243-303): GA over log10(theta) in cfg.bounds_for(d), each
+// generation one device batch; theta-hat and the GaTrace bitwise those of the reference.
+inline DeviceFitResult fit_gp_detailed(const gpemu::Dataset& data, const gpemu::FitConfig& cfg,
+                                       std::span<AcceleratedBackend* const> backends) {
+  if (backends.empty()) throw gpemu::ValidationError("fit_gp_detailed: no backend");
+  const std::size_t d = data.d();
+  const auto bounds = cfg.bounds_for(d);
+  cfg.ga.validate();
+  std::vector<double> lo(d), hi(d);
+  for (std::size_t k = 0; k < d; ++k) {
+    lo[k] = bounds[k].first;
+    hi[k] = bounds[k].second;
+  }
+  const int G = static_cast<int>(backends.size());
+  const int per = (cfg.ga.population + G - 1) / G;
+  std::vector<std::unique_ptr<ProfileEvaluator>> evs;
+  std::vector<gpemu_plan*> plans;
+  for (auto* be : backends) {
+    const std::size_t slots = detail::fit_slots(be->context().get(), data, per);
+    evs.push_back(std::make_unique<ProfileEvaluator>(data, cfg.p, cfg.nugget, *be, slots));
+    plans.push_back(evs.back()->get());
+  }
+  const gpemu_ga_config ga = detail::ga_config(cfg.ga);
+  gpemu_fit_result r{};
+  std::vector<double> theta(d), tb(cfg.ga.generations), tg(static_cast<std::size_t>(cfg.ga.generations) * d);
+  gpemu_model* h = nullptr;
+  check(gpemu_fit_multi(plans.data(), G, lo.data(), hi.data(), &ga, cfg.seed, &r, theta.data(),
+                        nullptr, tb.data(), tg.data(), &h));
+  auto& ledger = backends[0]->ledger();  // budget() evaluations + the alpha solve_full
+  for (int i = 0; i < cfg.ga.budget(); ++i) {
+    ledger.add_r_build();
+    ledger.add_factorization();
+  }
+  ledger.add_triangular_solves(2ull * static_cast<std::uint64_t>(cfg.ga.budget()) + 2);
+  DeviceFitResult out;
+  out.model = detail::wrap_model(h, data, theta, cfg.p, cfg.nugget);
+  out.model.alpha.resize(data.n());
+  check(gpemu_model_alpha(h, out.model.alpha.data()));
+  out.jitter_max = r.jitter_max;
+  for (int g = 0; g < cfg.ga.generations; ++g)
+    out.trace.generations.push_back(gpemu::GaGenerationRecord{
+        tb[g], std::vector<double>(tg.begin() + static_cast<std::ptrdiff_t>(g * d),
+                                   tg.begin() + static_cast<std::ptrdiff_t>((g + 1) * d)),
+        static_cast<std::uint64_t>(g + 1) * static_cast<std::uint64_t>(cfg.ga.population)});
+  return out;
+}
+
+inline DeviceFitResult fit_gp_detailed(const gpemu::Dataset& data, const gpemu::FitConfig& cfg,
+                                       AcceleratedBackend& backend) {
+  AcceleratedBackend* one[1] = {&backend};
+  return fit_gp_detailed(data, cfg, std::span<AcceleratedBackend* const>(one, 1));
+}
+
+inline DeviceGpModel fit_gp(const gpemu::Dataset& data, const gpemu::FitConfig& cfg,
+                            AcceleratedBackend& backend) {
+  return fit_gp_detailed(data, cfg, backend).model;
+}
+
+namespace detail {
+inline void check_test_inputs(const gpemu::Matrix<double>& X, std::size_t d) {
+  if (X.cols() != d) throw gpemu::ValidationError("predict: test input dimension mismatch");
+}
+}  // namespace detail
+
+// predict (predictor.hpp:20-50) on the device model; `pool` is accepted for signature
+// compatibility (points are independent; the device computes all of them in one launch).
+// mse (optional): the kriging variance of each point.
+inline std::vector<double> predict(const DeviceGpModel& model, const gpemu::Matrix<double>& test_inputs,
+                                   gpemu::detail::ThreadPool* pool = nullptr,
+                                   std::vector<double>* mse = nullptr) {
+  (void)pool;
+  detail::check_test_inputs(test_inputs, model.dataset.d());
+  const std::size_t N = test_inputs.rows();
+  std::vector<double> yhat(N);
+  if (mse) mse->resize(N);
+  check(gpemu_predict(model.device->get(), test_inputs.data(), N, yhat.data(), mse ? mse->data() : nullptr));
+  return yhat;
+}
+
+// predict on a plain reference GpModel<double> (e.g. one assembled by the reference itself):
+// the model is imported to the device once per call.
+inline std::vector<double> predict(const gpemu::GpModel<double>& model,
+                                   const gpemu::Matrix<double>& test_inputs, AcceleratedBackend& backend,
+                                   std::vector<double>* mse = nullptr) {
+  detail::check_test_inputs(test_inputs, model.dataset.d());
+  const std::size_t n = model.dataset.n(), d = model.dataset.d();
+  if (model.alpha.size() != n || model.factor.lower.rows() != n)
+    throw gpemu::ValidationError("predict: model factor / alpha do not match its dataset");
+  const double sc[4] = {model.neg2_log_lik, model.mu_hat, model.sigma2_hat, model.factor.jitter_used};
+  gpemu_model* h = nullptr;
+  check(gpemu_model_import(backend.context().get(), model.dataset.inputs().data(), n, d,
+                           model.params.theta.data(), model.params.p, sc, model.factor.log_det,
+                           model.factor.lower.data(), model.alpha.data(), &h));
+  Model dev(h);
+  const std::size_t N = test_inputs.rows();
+  std::vector<double> yhat(N);
+  if (mse) mse->resize(N);
+  check(gpemu_predict(h, test_inputs.data(), N, yhat.data(), mse ? mse->data() : nullptr));
+  return yhat;
+}
+
+// predict_set (predictor.hpp:71-79).
+inline gpemu::PredictionSet predict_set(const DeviceGpModel& model, gpemu::Matrix<double> test_inputs,
+                                        std::span<const double> truth = {},
+                                        gpemu::detail::ThreadPool* pool = nullptr) {
+  gpemu::PredictionSet out;
+  out.predictions = predict(model, test_inputs, pool);
+  out.test_inputs = std::move(test_inputs);
+  if (!truth.empty()) out.sspe = gpemu::sspe(out.predictions, truth);
+  return out;
 }
 
 }  // namespace gpemu_b200

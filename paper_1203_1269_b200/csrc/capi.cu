@@ -320,7 +320,7 @@ struct gpemu_plan {
 struct gpemu_model {
   gpemu_ctx* ctx = nullptr;
   int n = 0, d = 0, NT = 0;
-  double p = 1.95, mu = 0.0, sigma2 = 0.0, vtv = 0.0, neg2 = 0.0, jitter = 0.0;
+  double p = 1.95, mu = 0.0, sigma2 = 0.0, vtv = 0.0, neg2 = 0.0, jitter = 0.0, log_det = 0.0;
   std::vector<double> theta;
   DevBuf<double> X, theta_d, alpha, tiles, u, v;
   // extension-mode workspace for the MSE (test-point row tiles)
@@ -647,6 +647,7 @@ gpemu_model* make_model(gpemu_plan* pl, int slot, const double* theta, const dou
   m->sigma2 = rec[REC_SIGMA2];
   m->vtv = rec[REC_VTV];
   m->jitter = rec[REC_JITTER];
+  m->log_det = rec[REC_LOGDET];
   m->theta.assign(theta, theta + pl->d);
   cudaStream_t s = pl->ctx->stream;
   m->X.alloc((size_t)pl->n * pl->d);
@@ -1896,6 +1897,110 @@ int gpemu_model_scalars(const gpemu_model* m, double* out) {
 int gpemu_model_destroy(gpemu_model* m) {
   release(m);
   return GPEMU_OK;
+}
+
+int gpemu_model_factor(gpemu_model* m, double* L_out, double* log_det) {
+  GPEMU_GUARD_BEGIN
+  if (!m) return set_error(GPEMU_VALIDATION, "model_factor: null model");
+  if (log_det) *log_det = m->log_det;
+  if (!L_out) return GPEMU_OK;
+  ck(cudaSetDevice(m->ctx->device), "cudaSetDevice");
+  cudaStream_t s = m->ctx->stream;
+  DevBuf<double> dL;
+  own(&m->ctx->stream, dL);
+  dL.alloc((size_t)m->n * m->n);
+  launch_tiles_to_rowmajor(m->tiles.p, m->n, m->NT, dL.p, s);
+  m->ctx->launches += 1;
+  ck(cudaGetLastError(), "tiles_to_rowmajor launch");
+  d2h_sync(L_out, dL.p, (size_t)m->n * m->n * sizeof(double), s, "D2H L");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_model_alpha(gpemu_model* m, double* alpha_out) {
+  GPEMU_GUARD_BEGIN
+  if (!m || !alpha_out) return set_error(GPEMU_VALIDATION, "model_alpha: null argument");
+  ck(cudaSetDevice(m->ctx->device), "cudaSetDevice");
+  d2h_sync(alpha_out, m->alpha.p, (size_t)m->n * sizeof(double), m->ctx->stream, "D2H alpha");
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
+int gpemu_model_import(gpemu_ctx* ctx, const double* X, size_t n, size_t d, const double* theta,
+                       double p, const double* scalars, double log_det, const double* L,
+                       const double* alpha, gpemu_model** out) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !X || !theta || !scalars || !L || !alpha || !out)
+    return set_error(GPEMU_VALIDATION, "model_import: null argument");
+  if (n < 1 || d < 1) return set_error(GPEMU_VALIDATION, "model_import: empty model");
+  if (d > 32) return set_error(GPEMU_CONFIG, "model_import: d = %zu exceeds the device limit 32", d);
+  int rc = validate_params(theta, d, p, 0.0);
+  if (rc) return rc;
+  rc = validate_unit_cube(X, n, d, "model_import");
+  if (rc) return rc;
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t s = ctx->stream;
+  auto* m = new gpemu_model();
+  m->ctx = ctx;
+  m->bind();
+  ctx_adopt(ctx);
+  try {
+    m->n = (int)n;
+    m->d = (int)d;
+    m->NT = (int)((n + TILE - 1) / TILE);
+    const int Npad = m->NT * TILE;
+    m->p = p;
+    m->neg2 = scalars[0];
+    m->mu = scalars[1];
+    m->sigma2 = scalars[2];
+    m->jitter = scalars[3];
+    m->log_det = log_det;
+    m->theta.assign(theta, theta + d);
+    m->X.alloc(n * d);
+    m->theta_d.alloc(d);
+    m->alpha.alloc(Npad);
+    m->tiles.alloc((size_t)num_tiles(m->NT) * TILE_ELEMS);
+    m->u.alloc(Npad);
+    m->v.alloc(Npad);
+    DevBuf<double> dL, ones, dvtv;
+    DevBuf<int> flags, counter, error;
+    own(&ctx->stream, dL, ones, dvtv);
+    own(&ctx->stream, flags, counter, error);
+    dL.alloc(n * n);
+    ones.alloc(n);
+    dvtv.alloc(1);
+    flags.alloc(m->NT);
+    counter.alloc(1);
+    error.alloc(1);
+    const std::vector<double> h1(n, 1.0);
+    ck(cudaMemcpyAsync(m->X.p, X, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D X");
+    ck(cudaMemcpyAsync(m->theta_d.p, theta, d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D theta");
+    ck(cudaMemsetAsync(m->alpha.p, 0, Npad * sizeof(double), s), "memset");
+    ck(cudaMemcpyAsync(m->alpha.p, alpha, n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D alpha");
+    ck(cudaMemsetAsync(m->u.p, 0, Npad * sizeof(double), s), "memset");
+    ck(cudaMemcpyAsync(dL.p, L, n * n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D L");
+    ck(cudaMemcpyAsync(ones.p, h1.data(), n * sizeof(double), cudaMemcpyHostToDevice, s), "H2D ones");
+    ck(cudaMemsetAsync(flags.p, 0, m->NT * sizeof(int), s), "memset");
+    ck(cudaMemsetAsync(error.p, 0, sizeof(int), s), "memset");
+    launch_rowmajor_to_tiles(dL.p, (int)n, m->NT, 0.0, m->tiles.p, s);
+    // v = L^-1 1 (the kriging MSE's GLS term) and v'v in the reference's dot order
+    launch_tile_trsv(m->tiles.p, m->NT, ones.p, nullptr, 0.0, (int)n, m->v.p, 0, flags.p, counter.p, 1,
+                     error.p, ctx->num_sms, s);
+    launch_dot_seq(m->v.p, m->v.p, (int)n, dvtv.p, s);
+    ctx->launches += 3;
+    ck(cudaGetLastError(), "model_import launch");
+    int err = 0;
+    ck(cudaMemcpyAsync(&m->vtv, dvtv.p, sizeof(double), cudaMemcpyDeviceToHost, s), "D2H vtv");
+    ck(cudaMemcpyAsync(&err, error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
+    ck(cudaStreamSynchronize(s), "model_import");
+    if (err) throw CudaError{"tile_trsv: dependency wait timed out (deadlock guard)"};
+  } catch (...) {
+    release(m);
+    throw;
+  }
+  *out = m;
+  return GPEMU_OK;
+  GPEMU_GUARD_END
 }
 
 int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, double* mse) {

@@ -67,6 +67,8 @@ void launch_finalize(const double* factors, size_t slot_stride, const double* bo
 // Row-major n x n (lower used) + jitter on diagonal -> tiled slot storage.
 void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, double* tiles,
                               cudaStream_t s);
+// dot_accumulate (matrix.hpp:64-69) on the device: one thread, the reference's order.
+void launch_dot_seq(const double* a, const double* b, int n, double* out, cudaStream_t s);
 // Tiled -> row-major lower with strict upper zeroed.
 void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s);
 // Blocked triangular solve on a tiled factor (kernels_trsv.cu, backend.hpp:129-153): forward

@@ -148,4 +148,16 @@ void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cud
   tiles_to_rowmajor_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(tiles, n, L);
 }
 
+// dot_accumulate (matrix.hpp:64-69): sequential double dot in the reference's element order.
+__global__ void dot_seq_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
+                               double* __restrict__ out) {
+  double s = 0.0;
+  for (int i = 0; i < n; ++i) s = __dadd_rn(s, __dmul_rn(a[i], b[i]));
+  *out = s;
+}
+
+void launch_dot_seq(const double* a, const double* b, int n, double* out, cudaStream_t s) {
+  dot_seq_kernel<<<1, 1, 0, s>>>(a, b, n, out);
+}
+
 }  // namespace gpemu_dev

@@ -77,7 +77,8 @@ EXPORTED_SYMBOLS = (
     "gpemu_ga_thetas", "gpemu_ga_tell", "gpemu_ga_status", "gpemu_refine_fit",
     "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
     "gpemu_ctx_mem_info", "gpemu_plan_bytes", "gpemu_ticket_order", "gpemu_ctx_num_sms",
-    "gpemu_eval_batch_multi", "gpemu_fit_multi",
+    "gpemu_eval_batch_multi", "gpemu_fit_multi", "gpemu_model_factor", "gpemu_model_import",
+    "gpemu_model_alpha",
 )
 
 
@@ -151,6 +152,10 @@ def lib():
     L.gpemu_refine_fit.argtypes = [_vp, _dp, _dp, _dp, C.c_double, C.c_int, _dp, _dp,
                                    C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_scalars.argtypes = [_vp, _dp]
+    L.gpemu_model_factor.argtypes = [_vp, _dp, _dp]
+    L.gpemu_model_alpha.argtypes = [_vp, _dp]
+    L.gpemu_model_import.argtypes = [_vp, _dp, _sz, _sz, _dp, C.c_double, _dp, C.c_double, _dp,
+                                     _dp, C.POINTER(_vp)]
     L.gpemu_ctx_mem_info.argtypes = [_vp, C.POINTER(_sz), C.POINTER(_sz)]
     L.gpemu_plan_bytes.argtypes = [_sz, _sz, _sz, C.c_int]
     L.gpemu_plan_bytes.restype = _sz

@@ -35,3 +35,20 @@ def test_reference_bench_sweep_on_b200(tmp_path):
     r = subprocess.run([exe, str(tmp_path / "sweep.csv")], capture_output=True, text=True, timeout=900)
     print(r.stdout[-6000:], r.stderr[-2000:])
     assert r.returncode == 0 and "ALL PASSED" in r.stdout
+
+
+@pytest.mark.gpu
+def test_reference_program_dropin_on_b200():
+    """A reference program switched by namespace only (tests/cpp/test_dropin.cpp): the
+    reference's call shapes for ProfileEvaluator / neg2_log_profile / model_at_theta /
+    fit_gp_detailed / predict on gpemu_b200:: with an AcceleratedBackend -- theta-hat and the
+    GA trace bitwise the reference's, the Ledger equal, model_alpha_residual <= 1e-6."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    exe = os.path.join(HERE, "cpp", "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("tests/cpp/test_dropin not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    print(r.stdout[-4000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "ALL PASSED" in r.stdout
