@@ -79,6 +79,13 @@ void d2h_sync(void* dst, const void* src, size_t bytes, cudaStream_t s, const ch
 
 constexpr double kLadder[6] = {0.0, 1e-8, 1e-7, 1e-6, 1e-5, 1e-4};  // backend.hpp:77
 
+// Plans whose whole batch is a few tile tasks per SM (latency-bound passes: n <= 384 at 100
+// candidates) get a second set of slots for the speculative first ladder rung (run_batch).
+constexpr size_t kSpecTaskCap = 600;
+bool spec_slots_for(int NT, size_t max_batch) {
+  return (size_t)NT * (NT + 1) / 2 * max_batch <= kSpecTaskCap;
+}
+
 // Device memory: one stream-ordered pool per device, owned by the library, that keeps freed
 // blocks mapped (release threshold = max). A plan holds gigabytes (C3: 6.9 GB of factors and
 // table); cudaMalloc / cudaFree of those per plan cost 1-700 ms each on the box, more than the
@@ -280,6 +287,9 @@ struct gpemu_plan {
   std::vector<double> h_out;
   size_t last_B = 0;
   std::vector<int> last_ladder;  // ladder step per slot of the last batch (-1: failed)
+  std::vector<int> fslot;        // slot holding each candidate's factor in the last batch
+  bool spec_slots = false;       // speculation slots [max_batch + 1, 2 max_batch + 1) (run_batch)
+  bool spec_active = false;
   uint64_t r_builds = 0, factorizations = 0, solves = 0;
   // optional per-phase CUDA-event timing on the plan's stream (bench roofline)
   bool profile = false;
@@ -521,19 +531,46 @@ void run_chol(gpemu_plan* pl, int nact) {
 
 // Evaluates slots [0, B) whose thetas are already in pl->theta; runs the jitter
 // ladder (backend.hpp:105-119) on the device, re-assembling R only for the
-// candidates whose factorization failed. Leaves records in pl->out.
+// candidates whose factorization failed. Leaves records in pl->out[0, B) and the slot holding
+// each candidate's factor in pl->fslot.
 // With tolerate_nonfinite a slot with a non-finite R entry is left with its status-2 record
 // instead of failing the batch (speculative evaluations the caller may never use).
+//
+// Speculative first rung: on small designs a pass is bound by one candidate's serial chain,
+// not by throughput, so a retry pass costs a whole second chain. A plan with speculation slots
+// (kSpecTaskCap) evaluates, once the previous batch showed that most candidates climb the ladder,
+// every candidate at jitter 0 in slot i AND at kJitterLadder[1] in slot max_batch + 1 + i in the
+// same pass; a candidate that fails at 0 and succeeds at 1e-8 takes the second record and
+// factor (bitwise what the reference's second attempt computes: the same R + 1e-8 I through the
+// same kernels). Failures at both continue the ladder at 1e-7. One factorization per
+// candidate in the Ledger either way.
 int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
   cudaStream_t s = pl->ctx->stream;
   pl->last_B = B;
   pl->last_ladder.assign(B, -1);
+  pl->fslot.resize(B);
+  std::iota(pl->fslot.begin(), pl->fslot.end(), 0);
+  const char* spec_env = std::getenv("GPEMU_SPEC_LADDER");  // "0": off (A/B and tests)
+  const bool spec = pl->spec_slots && pl->spec_active && B <= pl->max_batch &&
+                    !(spec_env && spec_env[0] == '0');
+  const size_t SB = pl->max_batch + 1;  // first speculation slot
+  const size_t used = spec ? SB + B : B;
   std::vector<int> active(B);
   std::iota(active.begin(), active.end(), 0);
   for (size_t i = 0; i < B; ++i) pl->h_jitter[i] = 0.0;
-  ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), B * sizeof(double), cudaMemcpyHostToDevice, s),
+  if (spec) {
+    for (size_t i = 0; i < B; ++i) {
+      active.push_back((int)(SB + i));
+      pl->h_jitter[SB + i] = kLadder[1];
+    }
+    ck(cudaMemcpyAsync(pl->theta.p + SB * pl->d, pl->theta.p, B * pl->d * sizeof(double),
+                       cudaMemcpyDeviceToDevice, s),
+       "D2D speculation theta");
+  }
+  ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), used * sizeof(double), cudaMemcpyHostToDevice, s),
      "H2D jitter");
-  for (int step = 0; step < 6 && !active.empty(); ++step) {
+  std::vector<int> gather;  // (dst, src) record pairs of candidates resolved by speculation
+  for (int step = 0; step < 6 && !active.empty();) {
     const int nact = (int)active.size();
     if (step > 0) {
       for (int q = 0; q < nact; ++q) pl->h_jitter[active[q]] = kLadder[step];
@@ -573,24 +610,48 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
     nvtx_pop();
     pl->ctx->launches += 4;
     ck(cudaGetLastError(), "kernel launch");
-    ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, B * sizeof(int), cudaMemcpyDeviceToHost, s),
+    ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, used * sizeof(int), cudaMemcpyDeviceToHost, s),
        "D2H status");
     ck(cudaStreamSynchronize(s), "batch");
     std::vector<int> failed;
     for (int q = 0; q < nact; ++q) {
       const int slot = active[q];
+      if ((size_t)slot >= SB) continue;  // speculation slots are read with their candidate below
       const int st = pl->h_status_all[slot];
       if (st == 2) {
         if (tolerate_nonfinite) continue;
         return set_error(GPEMU_NONFINITE, "CorrelationPlan: non-finite correlation value");
       }
       if (st == 1) {
-        failed.push_back(slot);
+        if (spec && step == 0 && pl->h_status_all[SB + slot] == 0) {  // the second rung held
+          pl->last_ladder[slot] = 1;
+          pl->fslot[slot] = (int)(SB + slot);
+          gather.push_back(slot);
+          gather.push_back((int)(SB + slot));
+        } else {
+          failed.push_back(slot);
+        }
       } else {
         pl->last_ladder[slot] = step;
       }
     }
     active.swap(failed);
+    step += (spec && step == 0) ? 2 : 1;  // the speculative pass covered rungs 0 and 1
+  }
+  if (!gather.empty()) {  // records of the candidates resolved in their speculation slot
+    const int np = (int)gather.size() / 2;
+    std::copy(gather.begin(), gather.end(), pl->h_slots.begin());
+    ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), gather.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, s),
+       "H2D gather");
+    launch_copy_records(pl->out.p, pl->slots.p, np, s);
+    pl->ctx->launches += 1;
+  }
+  if (pl->spec_slots) {  // speculate while most candidates climb the ladder (GA generations are alike)
+    size_t climb = 0;
+    for (size_t i = 0; i < B; ++i) climb += pl->last_ladder[i] != 0;
+    if (!pl->spec_active && 2 * climb > B) pl->spec_active = true;
+    else if (pl->spec_active && 4 * climb < B) pl->spec_active = false;
   }
   int err = 0;
   d2h_sync(&err, pl->error.p, sizeof(int), pl->ctx->stream, "D2H error");
@@ -779,7 +840,7 @@ int gpemu_ctx_mem_info(gpemu_ctx* ctx, size_t* free_bytes, size_t* total_bytes) 
 size_t gpemu_plan_bytes(size_t n, size_t d, size_t max_batch, int precision) {
   const size_t NT = (n + TILE - 1) / TILE, tiles = NT * (NT + 1) / 2;
   const size_t elem = precision == GPEMU_PRECISION_SINGLE ? sizeof(float) : sizeof(double);
-  const size_t slots = max_batch + 1;
+  const size_t slots = (spec_slots_for((int)NT, max_batch) ? 2 * max_batch : max_batch) + 1;
   return tiles * TILE_ELEMS * (d * sizeof(double) + slots * elem) + slots * 2 * NT * TILE * elem +
          slots * (NT + 1) * NT * sizeof(int) + (n * d + n) * sizeof(double);
 }
@@ -1043,7 +1104,8 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
   pl->NT = (int)((n + TILE - 1) / TILE);
   pl->Npad = pl->NT * TILE;
   pl->max_batch = max_batch;
-  pl->nslots = max_batch + 1;
+  pl->spec_slots = spec_slots_for(pl->NT, max_batch);
+  pl->nslots = (pl->spec_slots ? 2 * max_batch : max_batch) + 1;
   pl->slot_stride = (size_t)num_tiles(pl->NT) * TILE_ELEMS;
   try {
     pl->X.alloc(n * d);
@@ -1225,15 +1287,16 @@ int gpemu_plan_last_factor(gpemu_plan* pl, size_t slot, double* L_out, double* l
   if (!pl) return set_error(GPEMU_VALIDATION, "last_factor: null plan");
   if (slot >= pl->last_B) return set_error(GPEMU_VALIDATION, "last_factor: slot %zu not in the last batch", slot);
   if (pl->last_ladder[slot] < 0) return set_error(GPEMU_NOT_PD, "last_factor: slot %zu did not factorize", slot);
+  const size_t fs = (size_t)pl->fslot[slot];  // the slot that holds this candidate's factor
   cudaStream_t s = pl->ctx->stream;
   if (L_out) {
     DevBuf<double> dL;
     own(&pl->ctx->stream, dL);
     dL.alloc((size_t)pl->n * pl->n);
     if (pl->precision == GPEMU_PRECISION_SINGLE)
-      launch_tiles_f32_to_rowmajor(pl->factors_f.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
+      launch_tiles_f32_to_rowmajor(pl->factors_f.p + fs * pl->slot_stride, pl->n, pl->NT, dL.p, s);
     else
-      launch_tiles_to_rowmajor(pl->factors.p + slot * pl->slot_stride, pl->n, pl->NT, dL.p, s);
+      launch_tiles_to_rowmajor(pl->factors.p + fs * pl->slot_stride, pl->n, pl->NT, dL.p, s);
     pl->ctx->launches += 1;
     ck(cudaMemcpyAsync(L_out, dL.p, (size_t)pl->n * pl->n * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H L");
   }
@@ -1498,7 +1561,7 @@ void eval_shard(gpemu_plan* pl, const double* thetas, int c0, int c1, double thr
         const double* r = &pl->h_out[(size_t)chunk_best * REC_SIZE];
         out->best = best;
         out->best_rec.assign(r, r + REC_SIZE);
-        if (keep) keep_factor(pl, chunk_best);
+        if (keep) keep_factor(pl, pl->fslot[chunk_best]);
       }
     }
   } catch (const CudaError& e) {
@@ -1840,7 +1903,7 @@ int gpemu_refine_fit_ex(gpemu_plan* pl, gpemu_plan* rebuild, const double* lo, c
       if (rc) return rc;
       download_records(rb, 1);
       if (std::isfinite(rb->h_out[REC_NEG2]) && rb->h_out[REC_NEG2] < neg2_fit) {
-        gpemu_model* m = make_model(rb, 0, theta.data(), rb->h_out.data());
+        gpemu_model* m = make_model(rb, rb->fslot[0], theta.data(), rb->h_out.data());
         if (scalars) {
           scalars[0] = m->neg2;
           scalars[1] = m->mu;
@@ -1868,7 +1931,7 @@ int gpemu_model_at_theta(gpemu_plan* pl, const double* theta, gpemu_model** mode
   const double* r = pl->h_out.data();
   if (!std::isfinite(r[REC_NEG2]))
     return set_error(GPEMU_NOT_PD, "model_at_theta: factorization failed at the requested theta");
-  gpemu_model* m = make_model(pl, 0, theta, r);
+  gpemu_model* m = make_model(pl, pl->fslot[0], theta, r);
   if (scalars) {
     scalars[0] = m->neg2;
     scalars[1] = m->mu;

@@ -67,6 +67,8 @@ void launch_finalize(const double* factors, size_t slot_stride, const double* bo
 // Row-major n x n (lower used) + jitter on diagonal -> tiled slot storage.
 void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, double* tiles,
                               cudaStream_t s);
+// out[pairs[2k]] = out[pairs[2k+1]] for k < np (REC_SIZE-double records).
+void launch_copy_records(double* out, const int* pairs, int np, cudaStream_t s);
 // dot_accumulate (matrix.hpp:64-69) on the device: one thread, the reference's order.
 void launch_dot_seq(const double* a, const double* b, int n, double* out, cudaStream_t s);
 // Tiled -> row-major lower with strict upper zeroed.

@@ -148,6 +148,18 @@ void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cud
   tiles_to_rowmajor_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(tiles, n, L);
 }
 
+// out[pairs[2k]] = out[pairs[2k + 1]] (whole records): candidates resolved in a speculation slot.
+__global__ void copy_records_kernel(double* __restrict__ out, const int* __restrict__ pairs, int np) {
+  const int k = blockIdx.x * blockDim.y + threadIdx.y;
+  if (k >= np || threadIdx.x >= REC_SIZE) return;
+  out[(size_t)pairs[2 * k] * REC_SIZE + threadIdx.x] = out[(size_t)pairs[2 * k + 1] * REC_SIZE + threadIdx.x];
+}
+
+void launch_copy_records(double* out, const int* pairs, int np, cudaStream_t s) {
+  const dim3 blk(REC_SIZE, 16);
+  copy_records_kernel<<<(np + 15) / 16, blk, 0, s>>>(out, pairs, np);
+}
+
 // dot_accumulate (matrix.hpp:64-69): sequential double dot in the reference's element order.
 __global__ void dot_seq_kernel(const double* __restrict__ a, const double* __restrict__ b, int n,
                                double* __restrict__ out) {

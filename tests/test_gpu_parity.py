@@ -675,3 +675,30 @@ def test_batch_invariance_across_kernel_instantiations(g, ctx):
         assert np.array_equal(big[k][40:48], small[k]), k
         assert np.array_equal(big[k][93:94], one[k]), k
     ev.close()
+
+
+def test_speculative_ladder_rung_bitwise(g, ctx, monkeypatch):
+    """C1 (every candidate climbs to 1e-8): once a batch showed that most candidates climb,
+    the next batches evaluate jitter 0 and 1e-8 in ONE pass (speculation slots). Records,
+    jitter steps, last_factor and the fit are bitwise those of the two-pass ladder."""
+    z = np.load(os.path.join(GOLD, "c1.npz"))
+    data = g.new_dataset(z["X"], z["y"])
+    be = g.Backend(ctx)
+    ev = g.ProfileEvaluator(data, 2.0, 0.0, be, max_batch=100)
+    first = ev.eval_batch(z["thetas"])  # two passes; arms the speculation
+    assert np.count_nonzero(first["jitter"] > 0) > 50
+    n0 = ctx.launch_count
+    second = ev.eval_batch(z["thetas"])
+    one_pass = ctx.launch_count - n0
+    L_spec = ev.last_factor(3).lower
+    monkeypatch.setenv("GPEMU_SPEC_LADDER", "0")
+    n0 = ctx.launch_count
+    third = ev.eval_batch(z["thetas"])
+    two_pass = ctx.launch_count - n0
+    L_plain = ev.last_factor(3).lower
+    assert one_pass < two_pass, (one_pass, two_pass)
+    for k in ("neg2", "mu", "sigma2", "jitter", "log_det", "status"):
+        assert np.array_equal(first[k], second[k]) and np.array_equal(second[k], third[k]), k
+    assert np.array_equal(L_spec, L_plain)
+    monkeypatch.delenv("GPEMU_SPEC_LADDER")
+    ev.close()
