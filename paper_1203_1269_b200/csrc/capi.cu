@@ -288,6 +288,7 @@ struct gpemu_plan {
   size_t last_B = 0;
   std::vector<int> last_ladder;  // ladder step per slot of the last batch (-1: failed)
   std::vector<int> fslot;        // slot holding each candidate's factor in the last batch
+  int h_error = 0;               // deadlock-guard word, read with each pass's statuses
   bool spec_slots = false;       // speculation slots [max_batch + 1, 2 max_batch + 1) (run_batch)
   bool spec_active = false;
   uint64_t r_builds = 0, factorizations = 0, solves = 0;
@@ -612,7 +613,9 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
     ck(cudaGetLastError(), "kernel launch");
     ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, used * sizeof(int), cudaMemcpyDeviceToHost, s),
        "D2H status");
+    ck(cudaMemcpyAsync(&pl->h_error, pl->error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
     ck(cudaStreamSynchronize(s), "batch");
+    if (pl->h_error) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
     std::vector<int> failed;
     for (int q = 0; q < nact; ++q) {
       const int slot = active[q];
@@ -653,9 +656,6 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
     if (!pl->spec_active && 2 * climb > B) pl->spec_active = true;
     else if (pl->spec_active && 4 * climb < B) pl->spec_active = false;
   }
-  int err = 0;
-  d2h_sync(&err, pl->error.p, sizeof(int), pl->ctx->stream, "D2H error");
-  if (err) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
   pl->r_builds += B;
   pl->factorizations += B;
   pl->solves += 2 * B;
