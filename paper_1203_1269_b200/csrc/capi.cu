@@ -187,6 +187,38 @@ struct DevBuf {
   ~DevBuf() { free(); }
 };
 
+// Page-locked host staging (per-pass slot lists, jitters, statuses, records): copies from and
+// to it are truly asynchronous and skip the driver's pageable bounce buffer, which matters for
+// the latency-bound small designs (a C1 batch is ~0.35 ms).
+template <typename T>
+struct PinnedVec {
+  T* p = nullptr;
+  size_t n = 0;
+  PinnedVec() = default;
+  PinnedVec(const PinnedVec&) = delete;
+  PinnedVec& operator=(const PinnedVec&) = delete;
+  ~PinnedVec() {
+    if (p) cudaFreeHost(p);
+  }
+  void assign(size_t count, T v) {
+    if (count > n) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      n = 0;
+      void* q = nullptr;
+      ck(cudaMallocHost(&q, (count ? count : 1) * sizeof(T)), "cudaMallocHost");
+      p = static_cast<T*>(q);
+      n = count;
+    }
+    std::fill(p, p + count, v);
+  }
+  T* data() { return p; }
+  const T* data() const { return p; }
+  T* begin() { return p; }
+  T& operator[](size_t i) { return p[i]; }
+  const T& operator[](size_t i) const { return p[i]; }
+};
+
 // Binds buffers to the stream their users launch on (see DevBuf).
 template <typename... B>
 void own(const cudaStream_t* s, B&... bufs) {
@@ -282,13 +314,13 @@ struct gpemu_plan {
   uint64_t data_hash = 0;  // FNV-1a of (n, d, X, y): plans of one dataset on several devices
   DevBuf<int> trsv_flags, trsv_counter;  // blocked triangular solve (alpha)
   int trsv_epoch = 0;
-  std::vector<double> h_jitter;
-  std::vector<int> h_slots, h_status_all;
-  std::vector<double> h_out;
+  PinnedVec<double> h_jitter;
+  PinnedVec<int> h_slots, h_status_all;
+  PinnedVec<double> h_out;
   size_t last_B = 0;
   std::vector<int> last_ladder;  // ladder step per slot of the last batch (-1: failed)
   std::vector<int> fslot;        // slot holding each candidate's factor in the last batch
-  int h_error = 0;               // deadlock-guard word, read with each pass's statuses
+  PinnedVec<int> h_error;        // deadlock-guard word, read with each pass's statuses
   bool spec_slots = false;       // speculation slots [max_batch + 1, 2 max_batch + 1) (run_batch)
   bool spec_active = false;
   uint64_t r_builds = 0, factorizations = 0, solves = 0;
@@ -570,7 +602,6 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
   }
   ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), used * sizeof(double), cudaMemcpyHostToDevice, s),
      "H2D jitter");
-  std::vector<int> gather;  // (dst, src) record pairs of candidates resolved by speculation
   for (int step = 0; step < 6 && !active.empty();) {
     const int nact = (int)active.size();
     if (step > 0) {
@@ -601,21 +632,22 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
     nvtx_pop();
     nvtx_push("K3 finalize");
     pl->mark_begin(2);
+    const int spec_off = (spec && step == 0) ? (int)SB : 0;  // records of rung 1 land in slot i
     if (pl->precision == GPEMU_PRECISION_SINGLE)
       launch_finalize_f32(pl->factors_f.p, pl->slot_stride, pl->borders_f.p, pl->status.p,
-                          pl->jitter.p, pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+                          pl->jitter.p, pl->n, pl->NT, pl->slots.p, nact, pl->out.p, spec_off, s);
     else
       launch_finalize(pl->factors.p, pl->slot_stride, pl->borders.p, pl->status.p, pl->jitter.p,
-                      pl->n, pl->NT, pl->slots.p, nact, pl->out.p, s);
+                      pl->n, pl->NT, pl->slots.p, nact, pl->out.p, spec_off, s);
     pl->mark_end();
     nvtx_pop();
     pl->ctx->launches += 4;
     ck(cudaGetLastError(), "kernel launch");
     ck(cudaMemcpyAsync(pl->h_status_all.data(), pl->status.p, used * sizeof(int), cudaMemcpyDeviceToHost, s),
        "D2H status");
-    ck(cudaMemcpyAsync(&pl->h_error, pl->error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
+    ck(cudaMemcpyAsync(pl->h_error.data(), pl->error.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H error");
     ck(cudaStreamSynchronize(s), "batch");
-    if (pl->h_error) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
+    if (pl->h_error[0]) return set_error(GPEMU_CUDA, "chol_dag: dependency wait timed out (deadlock guard)");
     std::vector<int> failed;
     for (int q = 0; q < nact; ++q) {
       const int slot = active[q];
@@ -628,9 +660,7 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
       if (st == 1) {
         if (spec && step == 0 && pl->h_status_all[SB + slot] == 0) {  // the second rung held
           pl->last_ladder[slot] = 1;
-          pl->fslot[slot] = (int)(SB + slot);
-          gather.push_back(slot);
-          gather.push_back((int)(SB + slot));
+          pl->fslot[slot] = (int)(SB + slot);  // its record is already in out[slot] (finalize)
         } else {
           failed.push_back(slot);
         }
@@ -640,15 +670,6 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
     }
     active.swap(failed);
     step += (spec && step == 0) ? 2 : 1;  // the speculative pass covered rungs 0 and 1
-  }
-  if (!gather.empty()) {  // records of the candidates resolved in their speculation slot
-    const int np = (int)gather.size() / 2;
-    std::copy(gather.begin(), gather.end(), pl->h_slots.begin());
-    ck(cudaMemcpyAsync(pl->slots.p, pl->h_slots.data(), gather.size() * sizeof(int),
-                       cudaMemcpyHostToDevice, s),
-       "H2D gather");
-    launch_copy_records(pl->out.p, pl->slots.p, np, s);
-    pl->ctx->launches += 1;
   }
   if (pl->spec_slots) {  // speculate while most candidates climb the ladder (GA generations are alike)
     size_t climb = 0;
@@ -917,7 +938,7 @@ static int factor_once(gpemu_ctx* ctx, gpemu_plan& pl, const double* dR, double 
   launch_rowmajor_to_tiles(dR, pl.n, pl.NT, jit, pl.factors.p, s);
   run_chol(&pl, 1);
   launch_finalize(pl.factors.p, pl.slot_stride, pl.borders.p, pl.status.p, pl.jitter.p, pl.n,
-                  pl.NT, pl.slots.p, 1, pl.out.p, s);
+                  pl.NT, pl.slots.p, 1, pl.out.p, 0, s);
   ctx->launches += 2;
   ck(cudaMemcpyAsync(st, pl.status.p, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
   ck(cudaMemcpyAsync(rec, pl.out.p, REC_SIZE * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
@@ -1083,7 +1104,6 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
   if (!ctx || !X || !y || !out) return set_error(GPEMU_VALIDATION, "plan_create: null argument");
   if (n < 2) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 2 design points");
   if (d < 1) return set_error(GPEMU_VALIDATION, "new_dataset: need at least 1 input dimension");
-  if (d > 32) return set_error(GPEMU_CONFIG, "plan_create: d = %zu exceeds the device table limit 32", d);
   if (max_batch < 1) return set_error(GPEMU_VALIDATION, "plan_create: max_batch must be >= 1");
   int rc = validate_unit_cube(X, n, d, "new_dataset");
   if (rc) return rc;
@@ -1161,6 +1181,7 @@ int gpemu_plan_create_ex(gpemu_ctx* ctx, const double* X, const double* y, size_
   pl->h_slots.assign(pl->nslots, 0);
   pl->h_status_all.assign(pl->nslots, 0);
   pl->h_out.assign(pl->nslots * REC_SIZE, 0.0);
+  pl->h_error.assign(1, 0);
   *out = pl;
   return GPEMU_OK;
   GPEMU_GUARD_END
@@ -1996,7 +2017,6 @@ int gpemu_model_import(gpemu_ctx* ctx, const double* X, size_t n, size_t d, cons
   if (!ctx || !X || !theta || !scalars || !L || !alpha || !out)
     return set_error(GPEMU_VALIDATION, "model_import: null argument");
   if (n < 1 || d < 1) return set_error(GPEMU_VALIDATION, "model_import: empty model");
-  if (d > 32) return set_error(GPEMU_CONFIG, "model_import: d = %zu exceeds the device limit 32", d);
   int rc = validate_params(theta, d, p, 0.0);
   if (rc) return rc;
   rc = validate_unit_cube(X, n, d, "model_import");

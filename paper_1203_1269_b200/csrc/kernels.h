@@ -59,16 +59,15 @@ size_t chol_dag_smem_bytes();
 
 // ---- K3: deviance (kernels_misc.cu) ----------------------------------------
 // ProfileEvaluator::eval tail (likelihood.hpp:124-140).
+// spec_off > 0: slots >= spec_off are speculation slots (layout.cuh spec_record_dst).
 void launch_finalize(const double* factors, size_t slot_stride, const double* borders,
                      const int* status, const double* jitter, int n, int NT, const int* slots,
-                     int nslots, double* out /*[slot][REC_SIZE]*/, cudaStream_t s);
+                     int nslots, double* out /*[slot][REC_SIZE]*/, int spec_off, cudaStream_t s);
 
 // ---- layout conversions / solves (kernels_misc.cu) -------------------------
 // Row-major n x n (lower used) + jitter on diagonal -> tiled slot storage.
 void launch_rowmajor_to_tiles(const double* A, int n, int NT, double jitter, double* tiles,
                               cudaStream_t s);
-// out[pairs[2k]] = out[pairs[2k+1]] for k < np (REC_SIZE-double records).
-void launch_copy_records(double* out, const int* pairs, int np, cudaStream_t s);
 // dot_accumulate (matrix.hpp:64-69) on the device: one thread, the reference's order.
 void launch_dot_seq(const double* a, const double* b, int n, double* out, cudaStream_t s);
 // Tiled -> row-major lower with strict upper zeroed.
@@ -120,7 +119,7 @@ void launch_chol_dag_f32(const DagLaunch& a, int num_sms, cudaStream_t s);
 size_t chol_dag_f32_smem_bytes();
 void launch_finalize_f32(const float* factors, size_t slot_stride, const float* borders,
                          const int* status, const double* jitter, int n, int NT, const int* slots,
-                         int nslots, double* out, cudaStream_t s);
+                         int nslots, double* out, int spec_off, cudaStream_t s);
 void launch_alpha_f32(const float* tiles, int n, const double* y, double mu, double* alpha, cudaStream_t s);
 void launch_tiles_f32_to_f64(const float* src, int NT, double* dst, cudaStream_t s);
 void launch_tiles_f32_to_rowmajor(const float* tiles, int n, int NT, double* L, cudaStream_t s);

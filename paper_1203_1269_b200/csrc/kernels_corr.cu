@@ -146,6 +146,59 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   }
 }
 
+// Any d (the d > 32 path): the same arithmetic as assemble_kernel -- s = fma(theta_k, T_k, s)
+// in ascending k, R = exp_neg(s), the same diagonal -- with the table and theta read from
+// global memory (L1-cached) instead of registers / shared memory.
+__global__ void __launch_bounds__(256) assemble_generic_kernel(
+    const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
+    double nugget, int NT, const int* __restrict__ slots, int nslots,
+    const double* __restrict__ jitter, double* __restrict__ factors, size_t slot_stride,
+    int* __restrict__ status) {
+  const int tile = blockIdx.x;
+  int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  while (I * (I + 1) / 2 > tile) --I;
+  const int J = tile - I * (I + 1) / 2;
+  const double* tb = table + (size_t)tile * d * TILE_ELEMS;
+  const double diag_base = __dadd_rn(1.0, nugget);
+  double* const fbase = factors + (size_t)tile * TILE_ELEMS;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    int r, c;
+    elem_rc(e, r, c);
+    const int i = I * TILE + r, j = J * TILE + c;
+    const bool pad = i >= n || j >= n;
+    double* dst = fbase + e;
+    if (pad || i == j) {
+      for (int si = 0; si < nslots; ++si) {
+        const int slot = slots[si];
+        dst[(size_t)slot * slot_stride] = pad ? (i == j ? 1.0 : 0.0) : __dadd_rn(diag_base, jitter[slot]);
+      }
+      continue;
+    }
+    for (int s0 = 0; s0 < nslots; s0 += kSlotILP) {
+      int sl[kSlotILP];
+      double sacc[kSlotILP];
+#pragma unroll
+      for (int q = 0; q < kSlotILP; ++q) {
+        sl[q] = slots[min(s0 + q, nslots - 1)];
+        sacc[q] = 0.0;
+      }
+      for (int k = 0; k < d; ++k) {
+        const double t = __ldg(tb + (size_t)k * TILE_ELEMS + e);
+#pragma unroll
+        for (int q = 0; q < kSlotILP; ++q) sacc[q] = fma(__ldg(theta + (size_t)sl[q] * d + k), t, sacc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kSlotILP; ++q) {
+        if (s0 + q >= nslots) break;
+        const double v = exp_neg(sacc[q]);
+        dst[(size_t)sl[q] * slot_stride] = v;
+        if (!isfinite(v) || isnan(sacc[q])) status[sl[q]] = 2;
+      }
+    }
+  }
+}
+
 template <int MAXD>
 static void launch_asm(dim3 grid, cudaStream_t s, const double* table, const double* theta, int n,
                        int d, double nugget, int NT, const int* slots, int nslots,
@@ -180,7 +233,10 @@ void launch_assemble(const double* table, const double* theta, const double* y, 
   else if (d <= 16) GPEMU_ASM(16);
   else if (d <= 20) GPEMU_ASM(20);
   else if (d <= 24) GPEMU_ASM(24);
-  else GPEMU_ASM(32);
+  else if (d <= 32) GPEMU_ASM(32);
+  else
+    assemble_generic_kernel<<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                                 factors, slot_stride, status);
 #undef GPEMU_ASM
 }
 

@@ -127,6 +127,43 @@ __global__ void __launch_bounds__(256) assemble_f32_kernel(
   }
 }
 
+// Any d (the d > 32 path): assemble_f32_kernel's arithmetic with the table and theta read from
+// global memory.
+__global__ void __launch_bounds__(256) assemble_f32_generic_kernel(
+    const double* __restrict__ table, const double* __restrict__ theta, int n, int d, double nugget,
+    int NT, const int* __restrict__ slots, int nslots, const double* __restrict__ jitter,
+    float* __restrict__ factors, size_t slot_stride, int* __restrict__ status) {
+  const int tile = blockIdx.x;
+  int I = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+  while ((I + 1) * (I + 2) / 2 <= tile) ++I;
+  while (I * (I + 1) / 2 > tile) --I;
+  const int J = tile - I * (I + 1) / 2;
+  const double* tb = table + (size_t)tile * d * TILE_ELEMS;
+  const float diag_base = 1.0f + (float)nugget;
+  float* const fbase = factors + (size_t)tile * TILE_ELEMS;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    const int c = e >> 7, r = e & 127;
+    const int i = I * TILE + r, j = J * TILE + c;
+    const bool pad = i >= n || j >= n;
+    float* dst = fbase + e;
+    for (int si = 0; si < nslots; ++si) {
+      const int slot = slots[si];
+      float v;
+      if (pad || i == j) {
+        v = pad ? (i == j ? 1.0f : 0.0f) : diag_base + (float)jitter[slot];
+      } else {
+        double sacc = 0.0;
+        for (int k = 0; k < d; ++k)
+          sacc = fma(__ldg(theta + (size_t)slot * d + k), __ldg(tb + (size_t)k * TILE_ELEMS + e), sacc);
+        const double ev = exp_neg(sacc);
+        v = (float)ev;
+        if (!isfinite(ev) || isnan(sacc)) status[slot] = 2;
+      }
+      dst[(size_t)slot * slot_stride] = v;
+    }
+  }
+}
+
 template <int MAXD>
 static void launch_asm_f(dim3 grid, cudaStream_t s, const double* table, const double* theta, int n,
                          int d, double nugget, int NT, const int* slots, int nslots,
@@ -168,7 +205,10 @@ void launch_assemble_f32(const double* table, const double* theta, const double*
   else if (d <= 16) GPEMU_ASMF(16);
   else if (d <= 20) GPEMU_ASMF(20);
   else if (d <= 24) GPEMU_ASMF(24);
-  else GPEMU_ASMF(32);
+  else if (d <= 32) GPEMU_ASMF(32);
+  else
+    assemble_f32_generic_kernel<<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots,
+                                                     jitter, factors, slot_stride, status);
 #undef GPEMU_ASMF
 }
 
@@ -179,7 +219,7 @@ constexpr int kLogChunkF = 2048;
 __global__ void __launch_bounds__(256) finalize_f32_kernel(
     const float* __restrict__ factors, size_t slot_stride, const float* __restrict__ borders,
     const int* __restrict__ status, const double* __restrict__ jitter, int n, int NT,
-    const int* __restrict__ slots, double* __restrict__ out) {
+    const int* __restrict__ slots, double* __restrict__ out, int spec_off) {
   __shared__ double logs[kLogChunkF];
   __shared__ double dots[3];
   const int slot = slots[blockIdx.x];
@@ -188,6 +228,8 @@ __global__ void __launch_bounds__(256) finalize_f32_kernel(
   const float* u = borders + (size_t)slot * 2 * Npad;
   const float* v = u + Npad;
   const int st = status[slot];
+  const int dst = spec_record_dst(status, slot, st, spec_off);
+  if (dst < 0) return;  // uniform
   double logsum = 0.0;
   if (st == 0) {
     for (int c0 = 0; c0 < n; c0 += kLogChunkF) {
@@ -211,7 +253,7 @@ __global__ void __launch_bounds__(256) finalize_f32_kernel(
     __syncthreads();
   }
   if (threadIdx.x != 0) return;
-  double* o = out + (size_t)slot * REC_SIZE;
+  double* o = out + (size_t)dst * REC_SIZE;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   o[REC_NEG2] = inf;
   o[REC_MU] = 0.0;
@@ -249,9 +291,9 @@ __global__ void __launch_bounds__(256) finalize_f32_kernel(
 
 void launch_finalize_f32(const float* factors, size_t slot_stride, const float* borders,
                          const int* status, const double* jitter, int n, int NT, const int* slots,
-                         int nslots, double* out, cudaStream_t s) {
+                         int nslots, double* out, int spec_off, cudaStream_t s) {
   finalize_f32_kernel<<<nslots, 256, 0, s>>>(factors, slot_stride, borders, status, jitter, n, NT,
-                                             slots, out);
+                                             slots, out, spec_off);
 }
 
 // alpha = solve_full(factor, y - mu) in float (likelihood.hpp:228-229, backend.hpp:129-169):
@@ -363,10 +405,39 @@ __global__ void __launch_bounds__(128) predict_f32_kernel(const double* __restri
   }
 }
 
+// Any d (the d > 32 path): predict_f32_kernel's float arithmetic from global-memory coordinates.
+__global__ void __launch_bounds__(128) predict_f32_generic_kernel(const double* __restrict__ Xt, int N,
+                                                                 const double* __restrict__ X, int n, int d,
+                                                                 const double* __restrict__ theta, double p,
+                                                                 double mu, const double* __restrict__ alpha,
+                                                                 double* __restrict__ yhat, int* bad) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jc = min(j, N - 1);
+  const float pf = (float)p;
+  double acc = 0.0;
+  bool nonfinite = false;
+  for (int r = 0; r < n; ++r) {
+    float s = 0.0f;
+    for (int k = 0; k < d; ++k)
+      s = fmaf((float)__ldg(theta + k),
+               pow_abs_f((float)__ldg(Xt + (size_t)jc * d + k) - (float)__ldg(X + (size_t)r * d + k), pf), s);
+    const float v = expf(-s);
+    nonfinite |= !isfinite(v);
+    acc = __dadd_rn(acc, __dmul_rn((double)v, __ldg(alpha + r)));
+  }
+  if (j < N) {
+    yhat[j] = mu + acc;
+    if (nonfinite) *bad = 1;
+  }
+}
+
 void launch_predict_f32(const double* Xt, int N, const double* X, int n, int d, const double* theta,
                         double p, double mu, const double* alpha, double* yhat, int* bad, cudaStream_t s) {
   if (N <= 0) return;
-  predict_f32_kernel<<<(N + 127) / 128, 128, 0, s>>>(Xt, N, X, n, d, theta, p, mu, alpha, yhat, bad);
+  if (d > 32)
+    predict_f32_generic_kernel<<<(N + 127) / 128, 128, 0, s>>>(Xt, N, X, n, d, theta, p, mu, alpha, yhat, bad);
+  else
+    predict_f32_kernel<<<(N + 127) / 128, 128, 0, s>>>(Xt, N, X, n, d, theta, p, mu, alpha, yhat, bad);
 }
 
 }  // namespace gpemu_dev

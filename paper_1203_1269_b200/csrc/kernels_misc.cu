@@ -26,7 +26,7 @@ constexpr int kLogChunk = 1024;
 __global__ void __launch_bounds__(256) finalize_kernel(
     const double* __restrict__ factors, size_t slot_stride, const double* __restrict__ borders,
     const int* __restrict__ status, const double* __restrict__ jitter, int n, int NT,
-    const int* __restrict__ slots, double* __restrict__ out) {
+    const int* __restrict__ slots, double* __restrict__ out, int spec_off) {
   __shared__ double logs[kLogChunk], su[kLogChunk], sv[kLogChunk];
   __shared__ double sums[4];
   const int slot = slots[blockIdx.x];
@@ -35,6 +35,8 @@ __global__ void __launch_bounds__(256) finalize_kernel(
   const double* u = borders + (size_t)slot * 2 * Npad;
   const double* v = u + Npad;
   const int st = status[slot];
+  const int dst = spec_record_dst(status, slot, st, spec_off);
+  if (dst < 0) return;  // uniform
   if (st == 0) {
     double acc = 0.0;  // warp 1 lane 0: logsum; warp 0 lanes 0..2: utu, vtu (v.u), vtv
     const int t = threadIdx.x;
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(
   const double logsum = st == 0 ? sums[3] : 0.0;
   const double dots[3] = {st == 0 ? sums[0] : 0.0, st == 0 ? sums[1] : 0.0, st == 0 ? sums[2] : 0.0};
   if (threadIdx.x != 0) return;
-  double* o = out + (size_t)slot * REC_SIZE;
+  double* o = out + (size_t)dst * REC_SIZE;
   const double inf = __longlong_as_double(0x7ff0000000000000LL);
   o[REC_NEG2] = inf;
   o[REC_MU] = 0.0;
@@ -101,9 +103,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(
 
 void launch_finalize(const double* factors, size_t slot_stride, const double* borders,
                      const int* status, const double* jitter, int n, int NT, const int* slots,
-                     int nslots, double* out, cudaStream_t s) {
+                     int nslots, double* out, int spec_off, cudaStream_t s) {
   finalize_kernel<<<nslots, 256, 0, s>>>(factors, slot_stride, borders, status, jitter, n, NT,
-                                         slots, out);
+                                         slots, out, spec_off);
 }
 
 // ---------------------------------------------------------------------------
@@ -146,18 +148,6 @@ __global__ void tiles_to_rowmajor_kernel(const double* __restrict__ tiles, int n
 
 void launch_tiles_to_rowmajor(const double* tiles, int n, int NT, double* L, cudaStream_t s) {
   tiles_to_rowmajor_kernel<<<dim3((n + 255) / 256, n), 256, 0, s>>>(tiles, n, L);
-}
-
-// out[pairs[2k]] = out[pairs[2k + 1]] (whole records): candidates resolved in a speculation slot.
-__global__ void copy_records_kernel(double* __restrict__ out, const int* __restrict__ pairs, int np) {
-  const int k = blockIdx.x * blockDim.y + threadIdx.y;
-  if (k >= np || threadIdx.x >= REC_SIZE) return;
-  out[(size_t)pairs[2 * k] * REC_SIZE + threadIdx.x] = out[(size_t)pairs[2 * k + 1] * REC_SIZE + threadIdx.x];
-}
-
-void launch_copy_records(double* out, const int* pairs, int np, cudaStream_t s) {
-  const dim3 blk(REC_SIZE, 16);
-  copy_records_kernel<<<(np + 15) / 16, blk, 0, s>>>(out, pairs, np);
 }
 
 // dot_accumulate (matrix.hpp:64-69): sequential double dot in the reference's element order.

@@ -75,6 +75,37 @@ __global__ void __launch_bounds__(kPredThreads, MAXD <= 12 ? 6 : 4) predict_kern
   }
 }
 
+// Any d (the d > 32 path): predict_kernel's arithmetic and summation order, coordinates and
+// theta read from global memory (the training row is the same address across the block).
+__global__ void __launch_bounds__(kPredThreads) predict_generic_kernel(
+    const double* __restrict__ Xt, int N, const double* __restrict__ X, int n, int d,
+    const double* __restrict__ theta, double p, const double* __restrict__ alpha,
+    double* __restrict__ part, int* bad) {
+  const int j = blockIdx.x * kPredThreads + threadIdx.x;
+  const int jc = min(j, N - 1);
+  const double* xt = Xt + (size_t)jc * d;
+  const int i0 = blockIdx.y * kTrainBlock, i1 = min(n, i0 + kTrainBlock);
+  double acc = 0.0;
+  bool nonfinite = false;
+  for (int c0 = i0; c0 < i1; c0 += kTrainStage) {
+    const int cn = min(kTrainStage, i1 - c0);
+    double tacc = 0.0;
+    for (int r = 0; r < cn; ++r) {
+      const double* xr = X + (size_t)(c0 + r) * d;
+      double s = 0.0;
+      for (int k = 0; k < d; ++k) s = __dadd_rn(s, __dmul_rn(__ldg(theta + k), pow_abs_p(xt[k] - __ldg(xr + k), p)));
+      const double v = exp_neg(s);
+      nonfinite |= !isfinite(v) || isnan(s);
+      tacc = fma(v, __ldg(alpha + c0 + r), tacc);
+    }
+    acc = __dadd_rn(acc, tacc);
+  }
+  if (j < N) {
+    part[(size_t)blockIdx.y * N + j] = acc;
+    if (nonfinite) *bad = 1;
+  }
+}
+
 __global__ void predict_combine_kernel(const double* __restrict__ part, int N, int nblk, double mu,
                                        double* __restrict__ yhat) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -112,7 +143,8 @@ void launch_predict(const double* Xt, int N, const double* X, int n, int d, cons
   else if (d <= 16) GPEMU_PRED(16);
   else if (d <= 20) GPEMU_PRED(20);
   else if (d <= 24) GPEMU_PRED(24);
-  else GPEMU_PRED(32);
+  else if (d <= 32) GPEMU_PRED(32);
+  else predict_generic_kernel<<<grid, kPredThreads, 0, s>>>(Xt, N, X, n, d, theta, p, alpha, part, bad);
 #undef GPEMU_PRED
   predict_combine_kernel<<<(N + 255) / 256, 256, 0, s>>>(part, N, nblk, mu, yhat);
 }
@@ -167,6 +199,31 @@ __global__ void __launch_bounds__(256) cross_tiles_kernel(const double* __restri
   if (nonfinite) *bad = 1;
 }
 
+// Any d (the d > 32 path): cross_tiles_kernel's arithmetic from global-memory coordinates.
+__global__ void __launch_bounds__(256) cross_tiles_generic_kernel(const double* __restrict__ Xt, int N,
+                                                                  const double* __restrict__ X, int n,
+                                                                  int d, const double* __restrict__ theta,
+                                                                  double p, int NT,
+                                                                  double* __restrict__ ext, int* bad) {
+  const int tile = blockIdx.x;
+  const int It = tile / NT, J = tile - It * NT;
+  double* out = ext + (size_t)tile * TILE_ELEMS;
+  bool nonfinite = false;
+  for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS; e += gridDim.y * blockDim.x) {
+    int r, c;
+    elem_rc(e, r, c);
+    const int pt = min(It * TILE + r, N - 1), pi = min(J * TILE + c, n - 1);
+    double s = 0.0;
+    for (int k = 0; k < d; ++k)
+      s = __dadd_rn(s, __dmul_rn(__ldg(theta + k), pow_abs_p(__ldg(Xt + (size_t)pt * d + k) - __ldg(X + (size_t)pi * d + k), p)));
+    const double v = exp_neg(s);
+    const bool live = It * TILE + r < N && J * TILE + c < n;
+    nonfinite |= live && (!isfinite(v) || isnan(s));
+    out[e] = live ? v : 0.0;
+  }
+  if (nonfinite) *bad = 1;
+}
+
 template <int MAXD>
 static void launch_cross(dim3 grid, cudaStream_t s, const double* Xt, int N, const double* X, int n,
                          int d, const double* theta, double p, int NT, double* ext, int* bad) {
@@ -192,7 +249,8 @@ void launch_cross_tiles(const double* Xt, int N, const double* X, int n, int d,
   else if (d <= 16) GPEMU_CROSS(16);
   else if (d <= 20) GPEMU_CROSS(20);
   else if (d <= 24) GPEMU_CROSS(24);
-  else GPEMU_CROSS(32);
+  else if (d <= 32) GPEMU_CROSS(32);
+  else cross_tiles_generic_kernel<<<grid, 256, 0, s>>>(Xt, N, X, n, d, theta, p, NT, ext, bad);
 #undef GPEMU_CROSS
 }
 

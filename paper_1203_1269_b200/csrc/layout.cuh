@@ -47,6 +47,16 @@ __host__ __device__ __forceinline__ size_t tile_index(int I, int J) {
 
 __host__ __device__ __forceinline__ int num_tiles(int NT) { return NT * (NT + 1) / 2; }
 
+// Record destination of a finalize block (the speculative first ladder rung, capi.cu run_batch):
+// with spec_off > 0, slot s >= spec_off evaluates candidate s - spec_off at jitter 1e-8 and
+// writes that candidate's record when its jitter-0 attempt failed (status 1) and this one held;
+// the base slot then writes nothing. -1: no record from this block.
+__host__ __device__ __forceinline__ int spec_record_dst(const int* status, int slot, int st, int spec_off) {
+  if (spec_off <= 0) return slot;
+  if (slot >= spec_off) return (status[slot - spec_off] == 1 && st == 0) ? slot - spec_off : -1;
+  return (st == 1 && status[slot + spec_off] == 0) ? -1 : slot;
+}
+
 // Per-slot result record (gpemu_eval_batch_device d_out layout).
 enum { REC_NEG2 = 0, REC_MU, REC_SIGMA2, REC_JITTER, REC_LOGDET, REC_STATUS, REC_UTU, REC_VTV,
        REC_SIZE };

@@ -152,3 +152,41 @@ def test_predict_shapes_vs_reference(g, ctx, orc, ref, ref_fast, n, d):
     y = gp_sample_path(orc, X, th_star, 1.95, rng)
     Xt = rng.random((500, d))
     _predict_case(g, ctx, orc, ref, ref_fast, X, y, th_star, 1.95, Xt, 100, 1e-7)
+
+
+@pytest.mark.parametrize("d", [33, 48])
+def test_dimension_above_32(g, ctx, orc, ref, ref_fast, d):
+    """d > 32 (the reference has no dimension limit): the generic assemble / predict /
+    cross-tile kernels against the compiled reference -- deviance records, the model's yhat
+    and the MSE -- and the float engine against the reference's float instantiation."""
+    rng = np.random.default_rng(d)
+    n = 600
+    X = random_lhd(n, d, rng)
+    y = np.sin(3 * X[:, :4]).sum(1) + 0.2 * X.sum(1)
+    th = 10 ** rng.uniform(-1.5, -0.5, size=(8, d))
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=8)
+    r = ev.eval_batch(th)
+    f = ref_fast.eval_batch(X, y, th, 1.95, threads=0)
+    s = ref.eval_batch(X, y, th, 1.95, threads=0)
+    assert np.array_equal(r["jitter"], f["jitter"])
+    self_disc = np.abs(f["neg2"] - s["neg2"]) / np.abs(f["neg2"])
+    assert np.all(np.abs(r["neg2"] - f["neg2"]) / np.abs(f["neg2"]) <= np.maximum(1e-9, 10 * self_disc))
+    ev.close()
+    Xt = rng.random((300, d))
+    _predict_case(g, ctx, orc, ref, ref_fast, X, y, th[0], 1.95, Xt, 100, 1e-7)
+    evs = g.ProfileEvaluator(g.new_dataset(X, y), 1.95, 0.0, g.Backend(ctx), max_batch=8,
+                             precision="single")
+    rs = evs.eval_batch(th)
+    fs = ref_fast.eval_batch(X, y, th, 1.95, threads=0, precision="single")
+    ref_err = np.abs(fs["neg2"] - f["neg2"]) / np.abs(f["neg2"])
+    same = rs["jitter"] == fs["jitter"]
+    assert same.sum() >= len(th) - 1
+    assert np.all((np.abs(rs["neg2"] - fs["neg2"]) / np.abs(fs["neg2"]))[same] <= np.maximum(1e-5, 10 * ref_err[same]))
+    m = g.model_at_theta(g.new_dataset(X, y), th[0], 1.95, 0.0, g.Backend(ctx), precision="single")
+    rf = ref_fast.model_predict(X, y, th[0], 1.95, 0.0, Xt, threads=0, precision="single")
+    rd = ref_fast.model_predict(X, y, th[0], 1.95, 0.0, Xt, threads=0)
+    scale = max(np.abs(rd["yhat"]).max(), np.abs(y).max())
+    ferr = np.abs(rf["yhat"] - rd["yhat"]).max() / scale
+    assert np.abs(g.predict(m, Xt) - rd["yhat"]).max() / scale <= max(1e-5, 3 * ferr)
+    evs.close()
+    m.close()
