@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_trsv_kernel(
       if constexpr (!upper) {
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
+#pragma unroll
           for (int o = 0; o < 32; ++o) {
             const int c = 32 * m + o;
             double xc = 0.0;
@@ -221,6 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1) tile_trsv_kernel(
       } else {
 #pragma unroll
         for (int m = 3; m >= 0; --m) {
+#pragma unroll
           for (int o = 31; o >= 0; --o) {
             const int j = 32 * m + o;
             double xj = 0.0;
