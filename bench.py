@@ -597,6 +597,17 @@ def main():
                 "inf_status_equal": bool(np.array_equal(np.isinf(dv["neg2"]), np.isinf(rj["neg2"]))),
                 "ref_neg2_bitwise_timed_vs_untimed": bool(np.array_equal(neg2, rj["neg2"])),
                 "against": "oracle/_ref libgpemu_ref_fast.so (the reference's headers, native flags)"}
+            if ref_available(fast=False):
+                # the reference disagrees with itself between its strict and native builds; the
+                # per-candidate gate is max(1e-9, 10x that self-discrepancy) (tests/test_gpu_parity.py)
+                rs = RefLib(fast=False).eval_batch(r["X"], r["y"], th, args.p, args.nugget, threads=0)
+                sd = np.abs(rs["neg2"][fin] - rj["neg2"][fin]) / np.abs(rj["neg2"][fin])
+                gate = np.maximum(1e-9, 10.0 * sd)
+                line["parity"].update({
+                    "gate": "max(1e-9, 10 x the reference's strict-vs-native-build self-discrepancy)",
+                    "max_rel_over_gate": float((rel / gate).max()) if rel.size else 0.0,
+                    "within_gate": bool(np.all(rel <= gate)),
+                    "max_ref_self_discrepancy": float(sd.max()) if sd.size else 0.0})
         else:
             line["cpu_baseline"] = None
     if rank == 0:
