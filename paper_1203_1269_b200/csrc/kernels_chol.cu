@@ -131,9 +131,16 @@ constexpr int kOffBar = kStages * kStageBytes;          // 192K: mbarriers
 constexpr int kOffW = kOffBar + 256;                    // border w: 2 x 128 doubles
 constexpr int kOffRinvD = kOffW + 2 * TILE * 8;        // 1 / L_cc of the DIAG tile
 constexpr int kOffMisc = kOffRinvD + TILE * 8;          // task scalars
-constexpr int kSmemBytes = kOffMisc + 64;
 constexpr long long kSpinLimitCycles = 20000000000LL;  // ~10 s: declare deadlock
 constexpr int kStageLd = 18;  // row stride (doubles) of the per-warp TRSM staging block
+// The OFF-task TRSM keeps its staging blocks and the packed diagonal blocks of L(j,j) above
+// the ring (L(j,j) itself occupies stages 0-1), so stage 2 stays free during the TRSM and
+// takes the next task's first slab.
+constexpr int kOffTrsmSt = kOffMisc + 128;                                  // [8 warps][16][kStageLd]
+constexpr int kTriElems = 136;                                              // packed 16x16 lower
+constexpr int kOffTrsmD = kOffTrsmSt + kConsumerWarps * 16 * kStageLd * 8;  // [8][kTriElems]
+constexpr int kSmemBytes = kOffTrsmD + 8 * kTriElems * 8;
+static_assert(kSmemBytes <= 227 * 1024, "shared memory");
 
 struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's registers)
   int ticket;
@@ -144,6 +151,9 @@ struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's 
   unsigned ljj_phase;  // uses of ljj_bar (the OFF-task L(j,j) load)
   int next;           // ticket taken ahead (prefetch of its seed tile), -1: none
   long long t_begin;   // PR_TOTAL start (profiling)
+  unsigned ready[16];  // K-tiles 1..255 whose operand flags were published at task start
+  int pre_next;        // the previous task issued slab 0 of ticket `next` into stage 2
+  int pre;             // this task's slab 0 is in stage 2 already
 };
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
@@ -286,6 +296,16 @@ __device__ __forceinline__ void stage_in(double (&acc)[2][16][2], const double* 
       acc[mi][nsub][0] = v.x;
       acc[mi][nsub][1] = v.y;
     }
+}
+
+// solve_row16 with D packed lower (row r at r(r+1)/2): the same operations in the same order.
+__device__ __forceinline__ void solve_row16p(double (&xr)[16], const double* D, const double* ri) {
+#pragma unroll
+  for (int c = 0; c < 16; ++c) {
+    xr[c] = div_by(xr[c], D[c * (c + 1) / 2 + c], ri[c]);
+#pragma unroll
+    for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] -= xr[c] * D[c2 * (c2 + 1) / 2 + c];
+  }
 }
 
 // One lane owns one row (16 values) of a block: X = B D^-T with D dense lower [16][16]
@@ -550,12 +570,16 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   }
   __syncthreads();
 
-  uint32_t it = 0;  // slab iteration counter, advanced identically by both roles
+  // Stage ring position, advanced identically by every thread: `cur` is the stage of the next
+  // slab, bit s of `ph` the parity of stage s's next completion.
+  int cur = 0;
+  uint32_t ph = 0;
 
   Prof pr{(a.prof && tid == 0) ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr, 0};
   if (tid == 0) {
     misc->ljj_phase = 0;
     misc->next = -1;
+    misc->pre_next = 0;
     misc->t_begin = clock64();
   }
   // Large batches take their next ticket when the mainloop ends and prefetch that task's R
@@ -572,6 +596,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   while (true) {
     if (tid == 0) {
       const int t = misc->next >= 0 ? misc->next : atomicAdd(a.counter, 1);
+      misc->pre = misc->next >= 0 ? misc->pre_next : 0;
+      misc->pre_next = 0;
       misc->next = -1;
       misc->ticket = t;
       misc->skip = 0;
@@ -587,7 +613,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         misc->bpos = bpos;
         misc->I = I;
         misc->j = j;
-        if (!ext) misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
+        // a prefetched slab 0 must be consumed (ring parity): such a task runs its mainloop
+        if (!ext && !misc->pre) misc->skip = *((volatile int*)&a.status[a.slots[bpos]]) != 0;
       }
     }
     __syncthreads();
@@ -667,10 +694,40 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // border rows (DIAG): running residual of [y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T
       double wacc = (diag && !skip) ? __ldcg(bord + brow * Npad + j * TILE + bc) : 0.0;
 
+      // Operand-flag snapshot: the last warp reads the flags of K-tiles 1..j-1 in one pass
+      // (lane = flag, acquire loads in parallel: one L2 round trip per 32 flags instead of two
+      // serial ones per K-tile in the producer), while thread 0 issues the prologue (K-tile 0,
+      // blocking wait). Published tiles are marked in misc->ready; their TMA loads are issued
+      // without touching the flags again, the rest take the blocking wait. The refill of slab
+      // 4 (K-tile 1) needs every warp past slab 1, so the bits are written by then (stage
+      // counter atomics after __threadfence_block order them). Short tasks (j < 8) keep the
+      // per-K-tile waits: their inputs are mostly unpublished at task start (n=1024: +2%).
+      if (warp == kConsumerWarps - 1 && j >= 8) {
+        const int kmax = j < 256 ? j : 256;
+        if (lane < 16) misc->ready[lane] = 0u;  // [0, 8): first flag, [8, 16): second flag
+        __syncwarp();
+        for (int e = lane; e < 2 * kmax - 2; e += 32) {
+          const int part = e >= kmax - 1;
+          const int K = 1 + e - part * (kmax - 1);
+          const int* f;
+          if (ext) {
+            f = &a.ext_flags[(size_t)It * NT + K];
+          } else if (part == 0) {
+            f = (slab_progress && diag && K == j - 1) ? nullptr : &flags[j * NT + K];
+          } else {
+            f = diag ? &flags[NT * NT + K] : &flags[I * NT + K];
+          }
+          if (f && ld_acquire_gpu(f) == epoch) atomicOr(&misc->ready[8 * part + (K >> 5)], 1u << (K & 31));
+        }
+        __syncwarp();
+      }
+
       // Thread 0 doubles as the TMA producer, kStages-1 slabs ahead of the math.
-      auto issue = [&](int p, uint32_t itp) {
+      auto issue = [&](int p, int stage) {
         const int K = p >> 2, sq = p & 3;
-        if (sq == 0) {
+        if (sq == 0 && j >= 8 && K > 0 && K < 256 && ((misc->ready[K >> 5] & misc->ready[8 + (K >> 5)]) >> (K & 31) & 1u)) {
+          fence_proxy_async_global();
+        } else if (sq == 0) {
           pr.start();
           const long long tw0 = (pr.p != nullptr || a.prof != nullptr) ? clock64() : 0;
           if (ext) {
@@ -694,7 +751,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           wait_flag_geq(&flags[(j - 1) * NT + j], 4 * epoch + sq + 1, a.error);
           fence_proxy_async_global();
         }
-        const int stage = itp % kStages;
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
         mbar_arrive_expect_tx(&full[stage], diag ? kSlabBytes + 2 * SLAB * 8 : kStageBytes);
         bulk_g2s(dst, a_tile(K) + sq * SLAB_ELEMS, kSlabBytes, &full[stage]);
@@ -710,20 +766,25 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       };
       // Prologue: the first kStages slabs. Afterwards the LAST warp to finish with a
       // stage refills it (slab q + kStages): no warp ever blocks waiting for the others.
+      // A task whose slab 0 the previous task issued into stage 2 starts the ring there.
+      const int pre = misc->pre;
+      if (pre) cur = 2;
       if (tid == 0) {
         const long long tsave = pr.last;
-        for (int p = 0; p < kStages && p < nslab; ++p) issue(p, it + p);
+        for (int p = pre; p < kStages && p < nslab; ++p) issue(p, cur + p < kStages ? cur + p : cur + p - kStages);
         pr.last = tsave;
       }
-      for (int q = 0; q < nslab; ++q, ++it) {
-        const int stage = it % kStages;
-        const uint32_t round = it / kStages;
+      for (int q = 0; q < nslab; ++q) {
+        const int stage = cur;
+        cur = cur == kStages - 1 ? 0 : cur + 1;
+        const uint32_t par = (ph >> stage) & 1u;
+        ph ^= 1u << stage;
         if (tid == 0 && pr.p) {
           const long long tw = clock64();
-          mbar_wait(&full[stage], round & 1);
+          mbar_wait(&full[stage], par);
           pr.p[PR_FULL_WAIT] += (unsigned long long)(clock64() - tw);
         } else {
-          mbar_wait(&full[stage], round & 1);
+          mbar_wait(&full[stage], par);
         }
         const double* As = reinterpret_cast<const double*>(smem + kOffStages + stage * kStageBytes);
         const double* Bs = diag ? As : As + SLAB_ELEMS;
@@ -780,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             if (q + kStages < nslab) {
               fence_proxy_async_shared();  // generic-proxy reads of the stage before the TMA write
               const long long tsave = pr.last;
-              issue(q + kStages, it + kStages);
+              issue(q + kStages, stage);
               pr.last = tsave;
             }
           }
@@ -797,6 +858,32 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           const double* seed = a.factors + (size_t)a.slots[bn] * a.slot_stride + tile_index(In, jn) * TILE_ELEMS;
 #pragma unroll
           for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4) bulk_prefetch_l2(seed + s4 * SLAB_ELEMS, kSlabBytes);
+          // After an OFF mainloop (its TRSM leaves stage 2 alone), the next task's slab 0 goes
+          // into stage 2 now if its K-tile-0 operands are published (non-blocking check), so
+          // that task starts without the flag round trips and the load latency.
+          const int sn = a.slots[bn];
+          if (!diag && jn > 0 && *((volatile int*)&a.status[sn]) == 0) {
+            const int* fln = a.flags + (size_t)sn * fstride;
+            const bool dn = In == jn;
+            if (ld_acquire_gpu(&fln[jn * NT]) == epoch &&
+                ld_acquire_gpu(dn ? &fln[NT * NT] : &fln[In * NT]) == epoch) {
+              fence_proxy_async_global();
+              fence_proxy_async_shared();  // generic-proxy reads of stage 2 before the TMA write
+              const double* facn = a.factors + (size_t)sn * a.slot_stride;
+              unsigned char* dst = smem + kOffStages + 2 * kStageBytes;
+              mbar_arrive_expect_tx(&full[2], dn ? kSlabBytes + 2 * SLAB * 8 : kStageBytes);
+              bulk_g2s(dst, facn + tile_index(In, 0) * TILE_ELEMS, kSlabBytes, &full[2]);
+              if (!dn) {
+                bulk_g2s(dst + kSlabBytes, facn + tile_index(jn, 0) * TILE_ELEMS, kSlabBytes, &full[2]);
+              } else {
+                const double* bn2 = a.borders + (size_t)sn * 2 * Npad;
+#pragma unroll
+                for (int r = 0; r < 2; ++r)
+                  bulk_g2s(dst + kSlabBytes + r * SLAB * 8, bn2 + r * Npad, SLAB * 8, &full[2]);
+              }
+              misc->pre_next = 1;
+            }
+          }
         }
       }
       if (tid == 0) {
@@ -903,13 +990,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           // The eight diagonal 16x16 blocks of L(j,j) are copied densely so the in-block
           // substitution reads them as warp-uniform (broadcast) loads with immediate offsets.
           double* rinv = W;
-          double* Dd = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);       // [8][16][16]
-          double* St = reinterpret_cast<double*>(smem + TILE_ELEMS * 8 + 2048 * 8) +
-                       warp * (16 * kStageLd);                                   // [16][kStageLd]
+          double* Dp = reinterpret_cast<double*>(smem + kOffTrsmD);              // [8][kTriElems]
+          double* St = reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * (16 * kStageLd);
           if (tid < TILE) rinv[tid] = 1.0 / Ls[elem_off(tid, tid)];
           for (int q = tid; q < 2048; q += kConsumers) {
             const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
-            Dd[q] = cc <= rr ? Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)] : 0.0;
+            if (cc <= rr) Dp[b8 * kTriElems + rr * (rr + 1) / 2 + cc] = Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)];
           }
           consumer_sync();
           // Fully unrolled over the eight 16-column blocks: window n-tiles w = 2cb, 2cb+1 are
@@ -927,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             if (lane < 16) {
               double xr[16];
               load_row16(xr, St + lane * kStageLd);
-              solve_row16(xr, Dd + cb * 256, rinv + o);
+              solve_row16p(xr, Dp + cb * kTriElems, rinv + o);
               store_row16(xr, St + lane * kStageLd);
             }
             __syncwarp();
