@@ -422,7 +422,7 @@ void release(H* h) {
 
 constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
 constexpr double kOrderQuantum = 0.0;  // us; ticket_order priority quantum (0: exact bottom level)
-constexpr double kOrderTail = 0.4;     // ticket_order: exact priority only below this fraction of the longest path
+constexpr double kOrderTail = 0.7;     // ticket_order: exact priority only below this fraction of the longest path
 
 // Ticket order for a large launch (B candidates x NT(NT+1)/2 tile tasks): a list schedule on
 // P processors with estimated task times (OFF(I,j): ~4 + 18.5 j + 20 us, DIAG(j): ~8 + 18.6 j
@@ -465,7 +465,7 @@ std::vector<int> ticket_order(int B, int NT, int P) {
     }
   }
   // Priority. Tasks whose bottom level is at least kOrderTail of the longest path (the first
-  // ~60% of every candidate's chain) share one key and go candidate-major (lower candidate,
+  // ~30% of every candidate's chain) share one key and go candidate-major (lower candidate,
   // then lower column, then lower row): a candidate's ready column group is dispatched together,
   // so the OFF(., j) tasks sharing the B panel L(j, 0..j-1) and the A panels of consecutive
   // columns are read through L2. Below that, the exact bottom level orders the tail, which is
@@ -473,7 +473,9 @@ std::vector<int> ticket_order(int B, int NT, int P) {
   // launch): exact bottom level everywhere 150.1 GB DRAM read, 5% L2 hits, 73.83 ms; with
   // kOrderTail = 0.4, 101.8 GB, 73.91 ms (same speed in alternating bench runs); candidate-major
   // everywhere 85.4 GB, +0.3%; the built-in column order 79.3 GB, +1.3%
-  // (tools/order_quantum_sweep.sh). GPEMU_ORDER_Q quantises the exact part (microseconds).
+  // (tools/order_quantum_sweep.sh). Round 2, with the operand-flag snapshot (GPEMU_ORDER_TAIL
+  // sweep, alternating runs): 0.7 is the best of {0, 0.2, 0.4, 0.55, 0.7, 0.85} over C3
+  // (73.26 ms vs 73.31 at 0.4), C2 (7.39 vs 7.53) and a 100-candidate n=1024 batch (2.09 vs 2.15). GPEMU_ORDER_Q quantises the exact part (microseconds).
   const char* qenv = std::getenv("GPEMU_ORDER_Q");
   const double quantum = qenv ? std::atof(qenv) : kOrderQuantum;
   struct Ready {
