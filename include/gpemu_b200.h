@@ -257,6 +257,15 @@ GPEMU_API int gpemu_model_destroy(gpemu_model* model);
  * (no reference implementation). Validates the unit cube. */
 GPEMU_API int gpemu_predict(gpemu_model* model, const double* Xtest, size_t N, double* yhat, double* mse);
 
+/* -- experiment.hpp --------------------------------------------------------- */
+/* maximin_lhd (experiment.hpp:142-172, DesignSpec :19-30): the random LHD and the swap draws on
+ * the host with the reference's RNG (detail/rng.hpp), the O(n^2 d) tracker and the
+ * exchange_budget swap scorings on the device. x_out: n x d row-major, bitwise the reference's
+ * design. min_dist (nullable): the design's minimum squared pairwise distance (NaN when no
+ * exchange ran: budget 0 or n == 2). */
+GPEMU_API int gpemu_maximin_lhd(gpemu_ctx* ctx, size_t n, size_t d, uint64_t seed, size_t exchange_budget,
+                                double* x_out, double* min_dist);
+
 #ifdef __cplusplus
 }
 #endif

@@ -554,6 +554,17 @@ inline std::vector<double> predict(const gpemu::GpModel<double>& model,
   return yhat;
 }
 
+// maximin_lhd (experiment.hpp:142-172) with the reference's DesignSpec: the random draws on the
+// host with the reference's RNG, the O(n^2 d) tracker and the swap scoring on the device. The
+// design is bitwise the reference's.
+inline gpemu::Matrix<double> maximin_lhd(const gpemu::DesignSpec& spec, AcceleratedBackend& backend) {
+  spec.validate();
+  gpemu::Matrix<double> x(spec.n, spec.d);
+  check(gpemu_maximin_lhd(backend.context().get(), spec.n, spec.d, spec.seed, spec.exchange_budget, x.data(),
+                          nullptr));
+  return x;
+}
+
 // predict_set (predictor.hpp:71-79).
 inline gpemu::PredictionSet predict_set(const DeviceGpModel& model, gpemu::Matrix<double> test_inputs,
                                         std::span<const double> truth = {},

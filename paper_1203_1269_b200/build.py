@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgpemu_b200.so")
 SOURCES = ["kernels_corr.cu", "kernels_chol.cu", "kernels_chol_f32.cu", "kernels_f32.cu", "kernels_misc.cu",
-           "kernels_predict.cu", "kernels_trsv.cu", "capi.cu"]
+           "kernels_predict.cu", "kernels_trsv.cu", "kernels_design.cu", "capi.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 EXTRA = os.environ.get("GPEMU_NVCC_EXTRA", "").split()
 FLAGS = EXTRA + ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

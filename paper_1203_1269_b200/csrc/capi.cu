@@ -2208,4 +2208,75 @@ int gpemu_predict(gpemu_model* m, const double* Xtest, size_t N, double* yhat, d
   GPEMU_GUARD_END
 }
 
+// maximin_lhd (experiment.hpp:142-172). The host side draws exactly what the reference draws,
+// in the same order, with the reference RNG's engine and output mappings (detail/rng.hpp:12-47:
+// splitmix64 seed derivation, std::mt19937_64, uniform01 = (u >> 11) 2^-53, Lemire's
+// below(n) = (u * n) >> 64): the random LHD (experiment.hpp:36-50), then (k, a, b) of every swap
+// (:155-158) -- the draws do not depend on acceptance. The device scores the swaps
+// (kernels_design.cu).
+int gpemu_maximin_lhd(gpemu_ctx* ctx, size_t n, size_t d, uint64_t seed, size_t exchange_budget,
+                      double* x_out, double* min_dist) {
+  GPEMU_GUARD_BEGIN
+  if (!ctx || !x_out) return set_error(GPEMU_VALIDATION, "maximin_lhd: null argument");
+  if (n < 2) return set_error(GPEMU_VALIDATION, "DesignSpec: n must be at least 2");
+  if (d < 1) return set_error(GPEMU_VALIDATION, "DesignSpec: d must be at least 1");
+  if (n > (size_t)INT32_MAX / 2 || d > 1000000 || exchange_budget > (size_t)INT32_MAX / 3)
+    return set_error(GPEMU_VALIDATION, "maximin_lhd: design too large");
+  NvtxRange range("maximin_lhd");
+  Rng rng(derive_seed(seed, 0x1d64ull));
+  // random_lhd: per column a Fisher-Yates permutation, then one uniform per point
+  std::vector<size_t> perm(n);
+  for (size_t k = 0; k < d; ++k) {
+    for (size_t i = 0; i < n; ++i) perm[i] = i;
+    for (size_t i = n - 1; i > 0; --i) std::swap(perm[i], perm[rng.below(i + 1)]);
+    for (size_t i = 0; i < n; ++i)
+      x_out[i * d + k] = (static_cast<double>(perm[i]) + rng.uniform01()) / static_cast<double>(n);
+  }
+  if (exchange_budget == 0 || n == 2) {  // nothing to exchange (experiment.hpp:147-149)
+    if (min_dist) *min_dist = std::nan("");
+    return GPEMU_OK;
+  }
+  std::vector<int> draws(3 * exchange_budget);
+  for (size_t it = 0; it < exchange_budget; ++it) {
+    const auto k = rng.below(d);
+    const auto a = rng.below(n);
+    auto b = rng.below(n - 1);
+    if (b >= a) ++b;
+    draws[3 * it] = (int)k;
+    draws[3 * it + 1] = (int)a;
+    draws[3 * it + 2] = (int)b;
+  }
+  ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t s = ctx->stream;
+  DevBuf<double> dX, dra, drb, res;
+  DevBuf<unsigned long long> r0, r1, red;
+  DevBuf<int> dD, fl;
+  own(&ctx->stream, dX, dra, drb, res, r0, r1, red, dD, fl);
+  dX.alloc(n * d);
+  dra.alloc(n);
+  drb.alloc(n);
+  res.alloc(2);
+  r0.alloc(n);
+  r1.alloc(n);
+  red.alloc(9);
+  dD.alloc(draws.size());
+  fl.alloc(n);
+  const unsigned long long inf = 0x7FF0000000000000ull;
+  const unsigned long long init[9] = {inf, inf, inf, 0, inf, inf, inf, 0, inf};
+  ck(cudaMemcpyAsync(dX.p, x_out, n * d * sizeof(double), cudaMemcpyHostToDevice, s), "H2D design");
+  ck(cudaMemcpyAsync(dD.p, draws.data(), draws.size() * sizeof(int), cudaMemcpyHostToDevice, s), "H2D draws");
+  ck(cudaMemcpyAsync(red.p, init, sizeof(init), cudaMemcpyHostToDevice, s), "H2D init");
+  gpemu_dev::MaximinLaunch L{dX.p, (int)n, (int)d, (int)exchange_budget, dD.p, r0.p, r1.p, dra.p, drb.p, fl.p,
+                             red.p, red.p + 8, res.p};
+  ck(gpemu_dev::launch_maximin(L, ctx->num_sms, s), "maximin launch");
+  ctx->launches += 2;
+  double hres[2];
+  ck(cudaMemcpyAsync(x_out, dX.p, n * d * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H design");
+  ck(cudaMemcpyAsync(hres, res.p, sizeof(hres), cudaMemcpyDeviceToHost, s), "D2H result");
+  ck(cudaStreamSynchronize(s), "maximin_lhd");
+  if (min_dist) *min_dist = hres[0];
+  return GPEMU_OK;
+  GPEMU_GUARD_END
+}
+
 }  // extern "C"

@@ -126,4 +126,22 @@ void launch_tiles_f32_to_rowmajor(const float* tiles, int n, int NT, double* L, 
 void launch_predict_f32(const double* Xt, int N, const double* X, int n, int d, const double* theta,
                         double p, double mu, const double* alpha, double* yhat, int* bad, cudaStream_t s);
 
+// ---- design generation (kernels_design.cu) --------------------------------------
+// maximin_lhd's tracker set-up and exchange loop (experiment.hpp:62-172) on a row-major n x d
+// design already on the device. draws: 3 ints (k, a, b) per swap from the reference's RNG.
+struct MaximinLaunch {
+  double* x;
+  int n, d, budget;
+  const int* draws;
+  unsigned long long* rmin0;  // per-row minimum distances (double bits), two buffers
+  unsigned long long* rmin1;
+  double* dra;                // new distances to the swapped rows
+  double* drb;
+  int* flist;                 // rows recomputed in full (<= n)
+  unsigned long long* red;    // 8 words, host-initialised {inf, inf, inf, 0} x 2
+  unsigned long long* init_min;  // global minimum of the start design, host-initialised to inf
+  double* result;             // [final minimum distance, accepted swaps]
+};
+cudaError_t launch_maximin(const MaximinLaunch& a, int num_sms, cudaStream_t s);
+
 }  // namespace gpemu_dev

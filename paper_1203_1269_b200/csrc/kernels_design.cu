@@ -1,0 +1,258 @@
+// kernels_design.cu -- maximin Latin-hypercube design on the device.
+//
+// Reference: experiment.hpp (relative to /root/reference/proj/include/gpemu/)
+//   squared_distance     :53-60    sequential sum over the d coordinates
+//   MinDistanceTracker   :62-130   pairwise distances with per-row minima
+//   maximin_lhd          :142-172  random LHD, then exchange_budget column-entry swaps, each kept
+//                                  only when it strictly raises the minimum pairwise distance
+//
+// The host draws the random LHD and every swap (k, a, b) with the reference's RNG (the draws do
+// not depend on acceptance); the device runs the O(n^2 d) tracker set-up and the exchange loop.
+// The reference keeps the n x n distance matrix (2 GB at n = 16384) and per-row argmins; here
+// only the per-row minima live on the device (O(n) state), and a swap is scored as:
+//   * rows r != a, b: the old and new distances to a and b are recomputed from x (O(d)); if the
+//     row's minimum was one of its old distances to a or b, the row is flagged and recomputed in
+//     full, otherwise its new minimum is min(old minimum, new d(r,a), new d(r,b)) -- exactly the
+//     reference's value (its argmin-based rule recomputes a subset of the flagged rows; on a tie
+//     the untouched argmin still carries the minimum, so both give the exact row minimum);
+//   * rows a and b: the minimum over the new d(r,a) (resp. d(r,b)) and d(a,b);
+//   * the swap is kept iff the global minimum (an exact min of the same doubles) strictly
+//     exceeds the current one, as `proposed > current` in the reference.
+// Every distance is the reference's sum in the reference's order with each product and sum
+// rounded separately (no FMA contraction: the strict build, oracle/_ref/libgpemu_ref.so), so the
+// accepted swaps -- and the design -- are bitwise the reference's.
+//
+// One cooperative kernel runs all the swaps: three grid barriers per swap (distances + flags |
+// flagged-row recomputes | decision). Minima are combined with 64-bit atomicMin on the bit
+// patterns (distances are positive doubles, whose bit patterns order like their values).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdlib>
+
+#include "kernels.h"
+
+namespace cg = cooperative_groups;
+
+namespace gpemu_dev {
+
+namespace {
+
+constexpr unsigned long long kInfBits = 0x7FF0000000000000ull;
+constexpr int kDesignThreads = 512;
+
+__device__ __forceinline__ unsigned long long dbits(double v) {
+  return static_cast<unsigned long long>(__double_as_longlong(v));
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+// squared_distance (experiment.hpp:53-60): s += diff * diff in coordinate order, every
+// operation rounded on its own.
+__device__ __forceinline__ double sqdist(const double* xr, const double* xc, int d) {
+  double s = 0.0;
+  for (int k = 0; k < d; ++k) {
+    const double diff = __dsub_rn(xr[k], xc[k]);
+    s = __dadd_rn(s, __dmul_rn(diff, diff));
+  }
+  return s;
+}
+
+// Block-wide min of v (every thread passes a value); the result is valid in thread 0.
+__device__ __forceinline__ double block_min(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red reuse
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    v = l < (int)(blockDim.x >> 5) ? red[l] : __longlong_as_double(kInfBits);
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  }
+  return v;
+}
+
+// MinDistanceTracker constructor (experiment.hpp:64-75): every row's minimum distance, and the
+// global minimum into *gmin. One thread per row; column rows are staged in shared memory.
+__global__ void __launch_bounds__(256) maximin_init_kernel(const double* __restrict__ x, int n, int d,
+                                                          unsigned long long* __restrict__ rmin,
+                                                          unsigned long long* __restrict__ gmin) {
+  extern __shared__ double xs[];  // [tr][d]
+  __shared__ double red[32];
+  const int tr = max(1, min(64, 6144 / d));
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  double m = __longlong_as_double(kInfBits);
+  for (int c0 = 0; c0 < n; c0 += tr) {
+    const int rows = min(tr, n - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < rows * d; e += blockDim.x) xs[e] = x[(size_t)c0 * d + e];
+    __syncthreads();
+    if (r < n) {
+      const double* xr = x + (size_t)r * d;
+      for (int i = 0; i < rows; ++i) {
+        if (c0 + i == r) continue;
+        m = fmin(m, sqdist(xr, xs + i * d, d));
+      }
+    }
+  }
+  if (r < n) rmin[r] = dbits(m);
+  const double bm = block_min(r < n ? m : __longlong_as_double(kInfBits), red);
+  if (threadIdx.x == 0) atomicMin(gmin, dbits(bm));
+}
+
+// The exchange loop (experiment.hpp:154-170). red[8]: two slots (by swap parity) of {min over
+// unflagged rows, row a's minimum, row b's minimum, flagged-row count}.
+__global__ void __launch_bounds__(kDesignThreads) maximin_exchange_kernel(MaximinLaunch a) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double red[32];
+  __shared__ double sdec;
+  const int n = a.n, d = a.d;
+  double* x = a.x;
+  const size_t gtid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t gsize = (size_t)gridDim.x * blockDim.x;
+  unsigned long long* cur = a.rmin0;
+  unsigned long long* nxt = a.rmin1;
+  double current = bitsd(*a.init_min);
+  int accepted = 0;
+  const double inf = __longlong_as_double(kInfBits);
+
+  for (int it = 0; it < a.budget; ++it) {
+    const int k = a.draws[3 * it], ia = a.draws[3 * it + 1], ib = a.draws[3 * it + 2];
+    unsigned long long* rs = a.red + 4 * (it & 1);
+    const double* xa = x + (size_t)ia * d;
+    const double* xb = x + (size_t)ib * d;
+    const double xak = xa[k], xbk = xb[k];
+
+    // ---- A: distances to the swapped rows; unflagged rows' new minima ----------------------
+    double lmin = inf, la = inf, lb = inf;
+    for (size_t r = gtid; r < (size_t)n; r += gsize) {
+      if ((int)r == ia || (int)r == ib) continue;
+      const double* xr = x + r * d;
+      double oa = 0.0, ob = 0.0, na = 0.0, nb = 0.0;
+      for (int kk = 0; kk < d; ++kk) {
+        const double xrk = xr[kk];
+        const double dao = __dsub_rn(xrk, xa[kk]), dbo = __dsub_rn(xrk, xb[kk]);
+        const double dan = kk == k ? __dsub_rn(xrk, xbk) : dao;  // row a after the swap holds x_b[k]
+        const double dbn = kk == k ? __dsub_rn(xrk, xak) : dbo;
+        oa = __dadd_rn(oa, __dmul_rn(dao, dao));
+        ob = __dadd_rn(ob, __dmul_rn(dbo, dbo));
+        na = __dadd_rn(na, __dmul_rn(dan, dan));
+        nb = __dadd_rn(nb, __dmul_rn(dbn, dbn));
+      }
+      a.dra[r] = na;
+      a.drb[r] = nb;
+      const double om = bitsd(cur[r]);
+      if (om == oa || om == ob) {  // the minimum may have left with the swap: recompute in B
+        a.flist[atomicAdd(&rs[3], 1ull)] = (int)r;
+        nxt[r] = kInfBits;
+      } else {
+        const double nm = fmin(om, fmin(na, nb));
+        nxt[r] = dbits(nm);
+        lmin = fmin(lmin, nm);
+      }
+      la = fmin(la, na);
+      lb = fmin(lb, nb);
+    }
+    double v = block_min(lmin, red);
+    if (threadIdx.x == 0) atomicMin(&rs[0], dbits(v));
+    v = block_min(la, red);
+    if (threadIdx.x == 0) atomicMin(&rs[1], dbits(v));
+    v = block_min(lb, red);
+    if (threadIdx.x == 0) atomicMin(&rs[2], dbits(v));
+    if (gtid == 0) {  // d(a, b) after the swap: experiment.hpp:90-92
+      double s = 0.0;
+      for (int kk = 0; kk < d; ++kk) {
+        const double diff = kk == k ? __dsub_rn(xbk, xak) : __dsub_rn(xa[kk], xb[kk]);
+        s = __dadd_rn(s, __dmul_rn(diff, diff));
+      }
+      atomicMin(&rs[1], dbits(s));
+      atomicMin(&rs[2], dbits(s));
+    }
+    grid.sync();
+
+    // ---- B: flagged rows in full; rows a and b; reset the other parity's slot -------------
+    const int m = (int)rs[3];
+    if (gtid == 0) {
+      nxt[ia] = rs[1];
+      nxt[ib] = rs[2];
+    }
+    if (gtid < 4) a.red[4 * ((it + 1) & 1) + gtid] = gtid < 3 ? kInfBits : 0ull;
+    for (int i = 0; i < m; ++i) {
+      const int r = a.flist[i];
+      const double* xr = x + (size_t)r * d;
+      double lm = inf;
+      for (size_t c = gtid; c < (size_t)n; c += gsize) {
+        if ((int)c == r) continue;
+        const double dv = (int)c == ia ? a.dra[r] : (int)c == ib ? a.drb[r] : sqdist(xr, x + c * d, d);
+        lm = fmin(lm, dv);
+      }
+      lm = block_min(lm, red);
+      if (threadIdx.x == 0) atomicMin(&nxt[r], dbits(lm));
+    }
+    grid.sync();
+
+    // ---- C: keep the swap iff the new global minimum is strictly larger -------------------
+    if (threadIdx.x == 0) {
+      double g = fmin(bitsd(rs[0]), fmin(bitsd(rs[1]), bitsd(rs[2])));
+      for (int i = 0; i < m; ++i) g = fmin(g, bitsd(nxt[a.flist[i]]));
+      sdec = g;
+    }
+    __syncthreads();
+    const double proposed = sdec;
+    if (proposed > current) {
+      current = proposed;
+      unsigned long long* t = cur;
+      cur = nxt;
+      nxt = t;
+      ++accepted;
+      if (gtid == 0) {
+        x[(size_t)ia * d + k] = xbk;
+        x[(size_t)ib * d + k] = xak;
+      }
+    }
+    grid.sync();
+  }
+  if (gtid == 0) {
+    a.result[0] = current;
+    a.result[1] = (double)accepted;
+  }
+}
+
+}  // namespace
+
+size_t maximin_init_smem(int d) {
+  const int tr = d < 6144 ? (6144 / d < 64 ? 6144 / d : 64) : 1;
+  return (size_t)tr * d * sizeof(double);
+}
+
+int maximin_grid(int n, int num_sms) {
+  const char* e = std::getenv("GPEMU_DESIGN_ROWS_PER_CTA");  // tuning override
+  const int rows = e ? std::atoi(e) : 512;  // 512: best of 256..4096 at n = 4096 and 16384
+  int g = (n + rows - 1) / (rows > 0 ? rows : 512);
+  if (g < 1) g = 1;
+  if (g > num_sms) g = num_sms;
+  return g;
+}
+
+cudaError_t launch_maximin(const MaximinLaunch& a, int num_sms, cudaStream_t s) {
+  const size_t smem = maximin_init_smem(a.d);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(maximin_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  maximin_init_kernel<<<(a.n + 255) / 256, 256, smem, s>>>(a.x, a.n, a.d, a.rmin0, a.init_min);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || a.budget == 0) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, maximin_exchange_kernel, kDesignThreads, 0);
+  if (e != cudaSuccess) return e;
+  int grid = maximin_grid(a.n, num_sms * (per_sm > 0 ? per_sm : 1));
+  MaximinLaunch args = a;
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)maximin_exchange_kernel, dim3(grid), dim3(kDesignThreads),
+                                     params, 0, s);
+}
+
+}  // namespace gpemu_dev

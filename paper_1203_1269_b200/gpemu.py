@@ -78,7 +78,7 @@ EXPORTED_SYMBOLS = (
     "gpemu_plan_create_ex", "gpemu_plan_precision", "gpemu_refine_fit_ex", "gpemu_model_scalars",
     "gpemu_ctx_mem_info", "gpemu_plan_bytes", "gpemu_ticket_order", "gpemu_ctx_num_sms",
     "gpemu_eval_batch_multi", "gpemu_fit_multi", "gpemu_model_factor", "gpemu_model_import",
-    "gpemu_model_alpha",
+    "gpemu_model_alpha", "gpemu_maximin_lhd",
 )
 
 
@@ -163,6 +163,7 @@ def lib():
                                       C.POINTER(C.c_int), C.POINTER(_vp), _dp, _dp]
     L.gpemu_model_destroy.argtypes = [_vp]
     L.gpemu_predict.argtypes = [_vp, _dp, _sz, _dp, _dp]
+    L.gpemu_maximin_lhd.argtypes = [_vp, _sz, _sz, C.c_uint64, _sz, _dp, _dp]
     _LIB = L
     return L
 
@@ -992,3 +993,34 @@ def sspe(predictions, truth) -> float:
         raise ValidationError("sspe: length mismatch")
     e = b - a
     return float(np.dot(e, e))
+
+
+# ---------------------------------------------------------------- experiment.hpp
+@dataclass
+class DesignSpec:
+    """experiment.hpp:19-30."""
+    n: int = 0
+    d: int = 0
+    seed: int = 0
+    exchange_budget: int = 10000
+
+    def validate(self):
+        if self.n < 2:
+            raise ValidationError("DesignSpec: n must be at least 2")
+        if self.d < 1:
+            raise ValidationError("DesignSpec: d must be at least 1")
+
+
+def maximin_lhd(spec: DesignSpec, ctx: Optional[Context] = None, return_min: bool = False):
+    """experiment.hpp:142-172: a random LHD and exchange_budget column-entry swaps, each kept only
+    when it strictly raises the minimum pairwise distance. The random draws run on the host with
+    the reference's RNG; the tracker and the swap scoring run on the device (kernels_design.cu).
+    Returns the n x d design (bitwise the reference's) and, with return_min, its minimum squared
+    pairwise distance (NaN when no exchange ran)."""
+    spec.validate()
+    ctx = ctx or default_context()
+    x = np.empty((spec.n, spec.d))
+    m = C.c_double(0.0)
+    _check(lib().gpemu_maximin_lhd(ctx.handle, spec.n, spec.d, C.c_uint64(spec.seed & (2**64 - 1)),
+                                   spec.exchange_budget, _p(x), C.byref(m)))
+    return (x, m.value) if return_min else x

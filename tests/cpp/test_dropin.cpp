@@ -7,11 +7,13 @@
 //   model_at_theta(data, theta, p, nugget, backend)                      likelihood.hpp:216-218
 //   fit_gp_detailed(data, cfg, backend) / fit_gp                         likelihood.hpp:243-308
 //   predict(model, test_inputs, pool)                                    predictor.hpp:20-22
+//   maximin_lhd(spec)                                                    experiment.hpp:142-172
 // with `gpemu::` -> `gpemu_b200::` and the backend an AcceleratedBackend; results are compared
 // with the reference's own ParallelBackend run of the same call (theta-hat and the GA trace
 // bitwise, the Ledger equal) and the reference's own model_alpha_residual is applied to the
 // device model. Test infrastructure: built by tests/cpp/Makefile, run by
 // tests/test_cpp_plugin.py (GPU).
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <initializer_list>
@@ -252,6 +254,22 @@ int main() {
     const std::vector<double> thc{2.0, 2.0};
     CHECK(gpemu_b200::model_at_theta(dc, thc, 1.95, 0.0, acc).factor.jitter_used ==
           model_at_theta<double>(dc, thc, 1.95, 0.0, *par).factor.jitter_used);
+  }
+
+  // design generation with the reference's DesignSpec: bitwise the reference's design
+  {
+    for (const DesignSpec spec : {DesignSpec{200, 2, 7, 10000}, DesignSpec{1500, 8, 3, 3000}, DesignSpec{2, 3, 1, 50}}) {
+      const auto t0 = std::chrono::steady_clock::now();
+      const Matrix<double> xr = maximin_lhd(spec);
+      const double tr = secs_since(t0);
+      const auto t1 = std::chrono::steady_clock::now();
+      const Matrix<double> xa = gpemu_b200::maximin_lhd(spec, acc);
+      const double ta = secs_since(t1);
+      CHECK(xa.rows() == xr.rows() && xa.cols() == xr.cols());
+      CHECK(std::equal(xa.data(), xa.data() + xa.rows() * xa.cols(), xr.data()));
+      std::printf("maximin_lhd n=%zu d=%zu budget=%zu: bitwise equal, reference %.3f s, device %.3f s\n", spec.n,
+                  spec.d, spec.exchange_budget, tr, ta);
+    }
   }
 
   // candidate sharding over two backends (two contexts; one device on this pool)
