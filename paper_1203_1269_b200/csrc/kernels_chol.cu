@@ -31,7 +31,7 @@
 //     its next ticket at mainloop end and bulk-prefetches that task's R tile into L2;
 //   * chol_dag_kernel<true> (B=1 models, refine batches: bound by each candidate's serial
 //     chain): the sub-diagonal tile L(j+1,j) is released slab by slab so DIAG(j+1)'s last
-//     k-step overlaps its TRSM, and the DIAG border chain is interleaved with its DMMAs.
+//     k-step overlaps its TRSM.
 //   Both produce bitwise the same factor.
 //
 // * chol_simple_kernel -- validation engine: one CTA per candidate, unblocked
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // tiles): the B operand is shared by all warps through shared memory, and every
       // row of the result stays in one warp, so the OFF-task TRSM needs no block barrier.
       const int lr = lane >> 2, lc = lane & 3;
-      const int brow = tid >> 7, bc = tid & 127;  // border accumulation role (DIAG)
+      const int brow = tid >> 7, bc = tid & 127;  // border solve role (DIAG)
       // tile (row I, col K): the factor's packed lower tiles, or the extension rows
       auto a_tile = [&](int K) -> double* {
         return ext ? a.ext + ((size_t)It * NT + K) * TILE_ELEMS : fac + tile_index(I, K) * TILE_ELEMS;
@@ -692,7 +692,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       }
       // border rows (DIAG): running residual of [y_j; 1_j] - sum_K [u_K; v_K] L(j,K)^T
-      double wacc = (diag && !skip) ? __ldcg(bord + brow * Npad + j * TILE + bc) : 0.0;
+      // as an 8 x 128 DMMA accumulator (rows 0/1 = u/v, rows 2..7 stay zero): warp w owns the
+      // border columns 16w..16w+15 (n-tiles 2w, 2w+1). Each k-step adds two DMMAs per warp;
+      // the per-thread 32-long FMA chain it replaces read the slab column-wise with 3x bank
+      // conflicts and made DIAG mainloops 1.8x slower than their DMMA bound.
+      double wb[2][2];
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn) {
+        const double2 v = (diag && !skip && lr < 2)
+                              ? __ldcg(reinterpret_cast<const double2*>(bord + lr * Npad + j * TILE + 16 * warp + 8 * nn + 2 * lc))
+                              : make_double2(0.0, 0.0);
+        wb[nn][0] = v.x;
+        wb[nn][1] = v.y;
+      }
 
       // Operand-flag snapshot: the last warp reads the flags of K-tiles 1..j-1 in one pass
       // (lane = flag, acquire loads in parallel: one L2 round trip per 32 flags instead of two
@@ -810,13 +822,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             const int ko = (ks ^ lr) << 2;
             const double a0 = -Aw0[ko], a1 = -Aw1[ko];
             const double* BwB = Bw - (warp + 1) * 256;  // slot sl > warp reads n-tile sl - warp - 1
-            // small launches: the border chain runs four columns per k-step ahead of the
-            // DMMAs, hidden under their issue (it is on the serial chain there)
-            if constexpr (kProgress) {
-              const double* ubp = As + SLAB_ELEMS + brow * SLAB;
-#pragma unroll
-              for (int k4 = 0; k4 < 4; ++k4)
-                wacc -= ubp[4 * ks + k4] * As[slab_off(bc, 4 * ks + k4)];
+            {  // border rows: [w_u; w_v] -= [u_K; v_K](k-step) L(j,K)(n-tiles 2w, 2w+1)^T
+              const double ab = lr < 2 ? -As[SLAB_ELEMS + lr * SLAB + 4 * ks + lc] : 0.0;
+              dmma884(wb[0][0], wb[0][1], ab, Bw[(2 * warp) * 256 + ko]);
+              dmma884(wb[1][0], wb[1][1], ab, Bw[(2 * warp + 1) * 256 + ko]);
             }
 #pragma unroll
             for (int sl = 0; sl < 17; ++sl) {
@@ -825,13 +834,6 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               dmma884(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1], first ? a0 : a1, b);
             }
           }
-        }
-        if (!kProgress && diag) {
-          // border rows: wacc -= sum_kk u_K[32 sq + kk] * L(j,K)[bc][32 sq + kk], the u_K
-          // segment from the stage (broadcast loads)
-          const double* ub = As + SLAB_ELEMS + brow * SLAB;
-#pragma unroll 8
-          for (int kk = 0; kk < SLAB; ++kk) wacc -= ub[kk] * Bs[slab_off(bc, kk)];
         }
         __syncwarp();
         if (lane == 0) {
@@ -903,11 +905,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           *reinterpret_cast<double2*>(C + acc_off(first ? rowA : rowB, first ? sl : sl - warp - 1, lc)) =
               make_double2(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1]);
         }
+        if (lr < 2) {
+#pragma unroll
+          for (int nn = 0; nn < 2; ++nn)
+            *reinterpret_cast<double2*>(W + lr * TILE + 16 * warp + 8 * nn + 2 * lc) = make_double2(wb[nn][0], wb[nn][1]);
+        }
         consumer_sync();
         if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
         if (!skip) {
-          W[brow * TILE + bc] = wacc;
           ok = diag_potrf(smem, C, rinvD, misc, warp, lane);
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
           consumer_sync();
