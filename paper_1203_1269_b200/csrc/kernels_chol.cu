@@ -1023,12 +1023,23 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               store_row16(xr, St + lane * kStageLd);
             }
             __syncwarp();
-            stage_in_at(acc, w, St, lr, lc);
             // (b) acc[:, a] -= X_block * L(j,j)[8a + lr, block cols]^T for the n-tiles a right
-            // of the block (element (8a + lr, o + 4ks + lc) of the swizzled tile layout)
+            // of the block (element (8a + lr, o + 4ks + lc) of the swizzled tile layout). The
+            // negated A fragments come straight from the solved block in St (one LDS each; the
+            // accumulator window is not reloaded: its columns are final and stored from St).
+            // (The chain-bound instantiation keeps the register route -- quad shuffles from the
+            // reloaded window -- which is 0.5% faster on a B=1 evaluation.)
+            if constexpr (kProgress) stage_in_at(acc, w, St, lr, lc);
             if (cb < 7) {
               double av[2][4];
-              window_afrags_at(acc, w, av, lane);
+              if constexpr (kProgress) {
+                window_afrags_at(acc, w, av, lane);
+              } else {
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                  for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -St[(8 * mi + lr) * kStageLd + 4 * ks + lc];
+              }
 #pragma unroll
               for (int ks = 0; ks < 4; ++ks) {
                 const double* Lk = Ls + ((cb >> 1) << 12) + lane_base +
@@ -1041,13 +1052,15 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
                 }
               }
             }
-            // (c) the block is final: store it
+            // (c) the block is final: store it from St
 #pragma unroll
             for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
               for (int nsub = 0; nsub < 2; ++nsub)
                 __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, w + nsub, lc)),
-                       make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1]));
+                       kProgress ? make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1])
+                                 : *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc));
+            if constexpr (!kProgress) __syncwarp();  // St is rewritten by the next block
             if (sub && (cb & 1) && cb < 7) {  // slab cb/2 of L(j+1, j) is final: release it
               consumer_sync();
               if (tid == 0) publish_flag(&flags[j * NT + I], 4 * epoch + (cb >> 1) + 1);
