@@ -154,6 +154,7 @@ struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's 
   unsigned ready[16];  // K-tiles 1..255 whose operand flags were published at task start
   int pre_next;        // the previous task issued slab 0 of ticket `next` into stage 2
   int pre;             // this task's slab 0 is in stage 2 already
+  int run;             // OFF task: the candidate was still unfailed at the TRSM start
 };
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
@@ -976,6 +977,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // the right, (c) store the finished block, (d) rotate the accumulator window.
         if (!skip) {
           if (tid == 0) {
+            misc->run = ext || *((volatile int*)&a.status[slot]) == 0;
             if (!ext) wait_flag(&flags[j * NT + j], epoch, a.error);
             fence_proxy_async_global();
             mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
@@ -987,8 +989,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           mbar_wait(ljj_bar, misc->ljj_phase & 1);
         }
         if (tid == 0) pr.lap(PR_OFF_WAIT);
-        bool run = !skip && (ext || *((volatile int*)&a.status[slot]) == 0);
-        if (sub) run = __syncthreads_and(run);  // uniform: the slab releases below are barriers
+        // uniform across the CTA (the TRSM below has CTA barriers): thread 0 read the status
+        // once before the L(j,j) load, and the load's mbarrier publishes it (a later DIAG of the
+        // same candidate may fail meanwhile: the TRSM then only does wasted work)
+        const bool run = !skip && misc->run != 0;
         if (run) {
           const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
           // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
