@@ -195,7 +195,7 @@ __device__ __forceinline__ void publish_flag(int* flag, int epoch) {
 enum {
   PR_TICKET = 0, PR_GEMM, PR_ACC_STORE, PR_POTRF, PR_DIAG_STORE, PR_BORDER, PR_OFF_WAIT, PR_TRSM,
   PR_OFF_STORE, PR_TASK_END, PR_PROD_FLAGS, PR_PROD_EMPTY, PR_N_DIAG, PR_N_OFF, PR_SLABS, PR_TOTAL,
-  PR_FULL_WAIT, PR_COUNT_USED
+  PR_FULL_WAIT, PR_DIAG_FULL_WAIT, PR_DIAG_GEMM, PR_COUNT_USED
 };
 constexpr int PR_COUNT = 24;
 struct Prof {
@@ -536,6 +536,51 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   return true;
 }
 
+// DIAG-task tile products: the 136 (m-tile, n-tile) pairs of the 128 x 128 lower triangle
+// (8 x 8 tiles) split into per-warp shapes whose operand addresses are a per-warp base plus
+// compile-time offsets (no per-slot selects in the mainloop):
+//   warps 0-3: a 4 x 4 block of the strictly-lower 64 x 64 quadrant (rows 8..15, cols 0..7);
+//   warps 4-5: the 4 x 4 off-diagonal block of the upper-left / lower-right 64 x 64 triangle;
+//   warps 6-7: the two 4-tile lower triangles on the diagonal of that triangle (20 products).
+// Each SMSP (warps w, w + 4) gets 32 or 36 products per k-step.
+__device__ __forceinline__ void diag_shape(int warp, int& m0, int& n0) {
+  if (warp < 4) {
+    m0 = 8 + 4 * (warp >> 1);
+    n0 = 4 * (warp & 1);
+  } else if (warp < 6) {
+    m0 = warp == 4 ? 4 : 12;
+    n0 = m0 - 4;
+  } else {
+    m0 = 8 * (warp - 6);
+    n0 = m0;
+  }
+}
+// accumulator slot -> (m-tile, n-tile); false for an unused slot. kShapes: the diag_shape split
+// (chain-bound launches: -2.4% on a C3 B=1 evaluation); otherwise warp w takes m-tiles w and
+// 15 - w (17 products; slot s <= w is (w, s), slot s > w is (15 - w, s - w - 1)), which is the
+// faster split in the throughput-bound instantiation (C2 -0.7%, n=1024 B=100 -1.4%).
+template <bool kShapes>
+__device__ __forceinline__ bool diag_slot_tile(int warp, int sl, int& m, int& n) {
+  if (!kShapes) {
+    const bool first = sl <= warp;
+    m = first ? warp : 15 - warp;
+    n = first ? sl : sl - warp - 1;
+    return sl < 17;
+  }
+  int m0, n0;
+  diag_shape(warp, m0, n0);
+  if (warp < 6) {
+    m = m0 + (sl >> 2);
+    n = n0 + (sl & 3);
+    return sl < 16;
+  }
+  const int t = sl >= 10 ? 1 : 0, q = sl - 10 * t;  // q -> (i, jj <= i) of a 4-tile triangle
+  const int i = q >= 6 ? 3 : q >= 3 ? 2 : q >= 1 ? 1 : 0;
+  m = m0 + 4 * t + i;
+  n = n0 + 4 * t + (q - i * (i + 1) / 2);
+  return sl < 20;
+}
+
 // kProgress: release sub-diagonal tiles slab by slab (small, chain-bound launches); the large-
 // launch instantiation carries none of that code.
 template <bool kProgress>
@@ -661,14 +706,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // `v -= L_it * L_jt` (backend.hpp:197-204), which keeps the rounding error
       // relative to the shrinking residual instead of the growing sum.
       // Row ownership: OFF tasks give warp w rows 16w..16w+15 (the TRSM needs whole rows per
-      // warp). DIAG tasks only need the lower triangle, so warp w takes the 8-row m-tiles w
-      // and 15 - w instead: every warp then computes 17 of the 32 n-tile products per k-step
-      // (the upper triangle is skipped, balanced across warps).
-      const int rowA = diag ? 8 * warp + lr : 16 * warp + lr;
-      const int rowB = diag ? 8 * (15 - warp) + lr : 16 * warp + 8 + lr;
-      // DIAG tasks use 17 accumulator slots s = 16 mi + ni, fixed at compile time: slot
-      // s <= warp is (m-tile w, n-tile s), slot s > warp is (m-tile 15 - w, n-tile s - w - 1), so
-      // the lower-triangle mainloop issues exactly 17 unpredicated DMMAs per k-step.
+      // warp). DIAG tasks only need the lower triangle: diag_shape splits its tile products.
+      const int rowA = 16 * warp + lr;
+      const int rowB = 16 * warp + 8 + lr;
+      // DIAG tasks: accumulator slots per diag_shape (16 or 20 tile products per warp).
       double acc[2][16][2];
       if (!diag) {
 #pragma unroll
@@ -683,11 +724,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       } else {
 #pragma unroll
         for (int sl = 0; sl < 32; ++sl) {
-          const bool first = sl <= warp;
-          const double2 v = (skip || sl >= 17)
-                                ? make_double2(0.0, 0.0)
-                                : __ldcg(reinterpret_cast<const double2*>(
-                                      gtile + acc_off(first ? rowA : rowB, first ? sl : sl - warp - 1, lc)));
+          int mt, nt;
+          const bool use = diag_slot_tile<kProgress>(warp, sl, mt, nt) && !skip;
+          const double2 v = use ? __ldcg(reinterpret_cast<const double2*>(gtile + acc_off(8 * mt + lr, nt, lc)))
+                                : make_double2(0.0, 0.0);
           acc[sl >> 4][sl & 15][0] = v.x;
           acc[sl >> 4][sl & 15][1] = v.y;
         }
@@ -795,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (tid == 0 && pr.p) {
           const long long tw = clock64();
           mbar_wait(&full[stage], par);
-          pr.p[PR_FULL_WAIT] += (unsigned long long)(clock64() - tw);
+          pr.p[diag ? PR_DIAG_FULL_WAIT : PR_FULL_WAIT] += (unsigned long long)(clock64() - tw);
         } else {
           mbar_wait(&full[stage], par);
         }
@@ -815,9 +855,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
             }
           }
-        } else {  // lower triangle only: m-tile w needs n-tiles 0..w, m-tile 15-w 0..15-w
-          const double* Aw0 = As + rowA * 32 + lc;
-          const double* Aw1 = As + rowB * 32 + lc;
+        } else if constexpr (!kProgress) {  // lower triangle only: m-tiles w and 15 - w
+          const double* Aw0 = As + (8 * warp + lr) * 32 + lc;
+          const double* Aw1 = As + (8 * (15 - warp) + lr) * 32 + lc;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             const int ko = (ks ^ lr) << 2;
@@ -833,6 +873,47 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
               const bool first = sl <= warp;
               const double b = (first ? Bw : BwB)[sl * 256 + ko];
               dmma884(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1], first ? a0 : a1, b);
+            }
+          }
+        } else {  // lower triangle only (diag_shape): B = A, the slab of L(j, K)
+          int m0, n0;
+          diag_shape(warp, m0, n0);
+          const double* Am = As + (8 * m0 + lr) * 32 + lc;
+          const double* Bn = As + (8 * n0 + lr) * 32 + lc;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            const int ko = (ks ^ lr) << 2;
+            {  // border rows: [w_u; w_v] -= [u_K; v_K](k-step) L(j,K)(n-tiles 2w, 2w+1)^T
+              const double ab = lr < 2 ? -As[SLAB_ELEMS + lr * SLAB + 4 * ks + lc] : 0.0;
+              dmma884(wb[0][0], wb[0][1], ab, Bw[(2 * warp) * 256 + ko]);
+              dmma884(wb[1][0], wb[1][1], ab, Bw[(2 * warp + 1) * 256 + ko]);
+            }
+            if (warp < 6) {  // 4 x 4 block
+              double am[4], bn[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                am[i] = -Am[i * 256 + ko];
+                bn[i] = Bn[i * 256 + ko];
+              }
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                  dmma884(acc[0][4 * i + jj][0], acc[0][4 * i + jj][1], am[i], bn[jj]);
+            } else {  // two 4-tile lower triangles on the diagonal (m0 = n0: A and B rows coincide)
+#pragma unroll
+              for (int t = 0; t < 2; ++t) {
+                double bt[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) bt[i] = Bn[(4 * t + i) * 256 + ko];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                  for (int jj = 0; jj <= i; ++jj) {
+                    const int sl = 10 * t + i * (i + 1) / 2 + jj;
+                    dmma884(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1], -bt[i], bt[jj]);
+                  }
+              }
             }
           }
         }
@@ -890,6 +971,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       }
       if (tid == 0) {
+        if (diag && pr.p) pr.p[PR_DIAG_GEMM] += (unsigned long long)(clock64() - pr.last);
         pr.lap(PR_GEMM);
         pr.add(PR_SLABS, nslab);
         pr.add(diag ? PR_N_DIAG : PR_N_OFF, 1);
@@ -901,10 +983,11 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // (non-inlined) function so its register pressure stays out of the mainloop
         // (the upper triangle of C is left as is: nothing downstream reads it)
 #pragma unroll
-        for (int sl = 0; sl < 17; ++sl) {
-          const bool first = sl <= warp;
-          *reinterpret_cast<double2*>(C + acc_off(first ? rowA : rowB, first ? sl : sl - warp - 1, lc)) =
-              make_double2(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1]);
+        for (int sl = 0; sl < 20; ++sl) {
+          int mt, nt;
+          if (diag_slot_tile<kProgress>(warp, sl, mt, nt))
+            *reinterpret_cast<double2*>(C + acc_off(8 * mt + lr, nt, lc)) =
+                make_double2(acc[sl >> 4][sl & 15][0], acc[sl >> 4][sl & 15][1]);
         }
         if (lr < 2) {
 #pragma unroll

@@ -616,7 +616,7 @@ class ProfileEvaluator:
 
     DAG_PHASES = ("ticket", "gemm", "acc_store", "potrf", "diag_store", "border", "off_wait",
                   "trsm", "off_store", "task_end", "prod_flags", "prod_empty", "n_diag", "n_off",
-                  "slabs", "total", "full_wait")
+                  "slabs", "total", "full_wait", "diag_full_wait", "diag_gemm")
 
     def dag_profile(self, enable: bool = True, read: bool = False):
         """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""
@@ -628,6 +628,7 @@ class ProfileEvaluator:
             return None
         m = out[:sms * 24].reshape(-1, 24)
         res = {k: m[:, i] for i, k in enumerate(self.DAG_PHASES)}
+        res["flag_wait_by_j"] = out[sms * 24:sms * 24 + 256]  # producer flag waits: [0,128) OFF, [128,256) DIAG, by j
         res["trace"] = out[sms * 24 + 256:].reshape(-1, 4)  # per ticket: start, gemm end, publish, end (ns)
         return res
 
