@@ -933,7 +933,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       }
       consumer_sync();  // every consumer is done reading the stage ring
       stamp(1);
-      if (take_ahead && tid == 0 && misc->ticket < ntasks - 2 * (int)gridDim.x) {
+      // Thread 0's post-mainloop work, in latency order: an OFF task's L(j,j) load goes out
+      // first (every warp waits for it), then the take-ahead of the next ticket -- several
+      // dependent L2 round trips (ticket, order table, slot, status, flags) that now overlap
+      // the L(j,j) transfer instead of preceding it.
+      auto take_next = [&]() {
+      if (take_ahead && misc->ticket < ntasks - 2 * (int)gridDim.x) {
         const int tn = atomicAdd(a.counter, 1);
         misc->next = tn;
         if (tn < ntasks) {
@@ -969,6 +974,20 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             }
           }
         }
+      }
+      };
+      if (tid == 0) {
+        if (!diag && !skip) {
+          misc->run = ext || *((volatile int*)&a.status[slot]) == 0;
+          if (!ext) wait_flag(&flags[j * NT + j], epoch, a.error);
+          fence_proxy_async_global();
+          mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
+          const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
+#pragma unroll
+          for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
+            bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, ljj_bar);
+        }
+        take_next();
       }
       if (tid == 0) {
         if (diag && pr.p) pr.p[PR_DIAG_GEMM] += (unsigned long long)(clock64() - pr.last);
@@ -1058,19 +1077,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // each warp then solves its own 16 rows in registers, 16 columns at a time:
         // (a) in-block substitution (quad shuffles), (b) DMMA update of the columns to
         // the right, (c) store the finished block, (d) rotate the accumulator window.
-        if (!skip) {
-          if (tid == 0) {
-            misc->run = ext || *((volatile int*)&a.status[slot]) == 0;
-            if (!ext) wait_flag(&flags[j * NT + j], epoch, a.error);
-            fence_proxy_async_global();
-            mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
-            const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
-#pragma unroll
-            for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
-              bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, ljj_bar);
-          }
-          mbar_wait(ljj_bar, misc->ljj_phase & 1);
-        }
+        if (!skip) mbar_wait(ljj_bar, misc->ljj_phase & 1);  // issued by thread 0 at mainloop end
         if (tid == 0) pr.lap(PR_OFF_WAIT);
         // uniform across the CTA (the TRSM below has CTA barriers): thread 0 read the status
         // once before the L(j,j) load, and the load's mbarrier publishes it (a later DIAG of the
