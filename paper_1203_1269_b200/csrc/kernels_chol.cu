@@ -195,7 +195,8 @@ __device__ __forceinline__ void publish_flag(int* flag, int epoch) {
 enum {
   PR_TICKET = 0, PR_GEMM, PR_ACC_STORE, PR_POTRF, PR_DIAG_STORE, PR_BORDER, PR_OFF_WAIT, PR_TRSM,
   PR_OFF_STORE, PR_TASK_END, PR_PROD_FLAGS, PR_PROD_EMPTY, PR_N_DIAG, PR_N_OFF, PR_SLABS, PR_TOTAL,
-  PR_FULL_WAIT, PR_DIAG_FULL_WAIT, PR_DIAG_GEMM, PR_COUNT_USED
+  PR_FULL_WAIT, PR_DIAG_FULL_WAIT, PR_DIAG_GEMM, PR_P_PIV, PR_P_BDW, PR_P_PANEL, PR_P_BPW, PR_P_UPD,
+  PR_COUNT_USED
 };
 constexpr int PR_COUNT = 24;
 struct Prof {
@@ -451,14 +452,31 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 
 
 // DIAG-task POTRF of the 128x128 tile C (tile layout in shared memory, = R - sum L L^T):
-// blocked right-looking in the register layout. Step kb: warp kb factors its 16x16
-// diagonal block in registers (one lane per row); warps below solve their panel block
-// against it (one lane per row) and publish it to a dense panel buffer; then each updates
-// its own trailing columns with DMMA. Finished blocks are written back into C. Returns
-// false on a failed pivot (uniform). Reciprocal pivots -> rinvD[0..127].
+// blocked right-looking in the register layout, warp w owning rows 16w..16w+15, with a one-
+// block look-ahead. Step kb: warp kb factors its 16x16 diagonal block in registers (one lane
+// per row) and releases it (named barrier BD); each warp w > kb solves its panel block against
+// it and publishes it to a dense panel buffer; warp kb+1 then updates only its own diagonal
+// block with its own panel and goes on to factor step kb+1 at once, while warps > kb+1 wait
+// for all step-kb panels (named barrier BP) and update their trailing columns with DMMA. The
+// serial chain per step is factor -> one panel solve -> one 16x16 update (the trailing
+// updates of the other warps run under the next factorization). Every element gets the same
+// operations in the same order as without the look-ahead. Pivot blocks and panels are double-
+// buffered by step parity (the barriers keep any warp within one step of its readers).
+// Finished blocks are written back into C. Reciprocal pivots -> rinvD[0..127]. Returns false
+// on a failed pivot (uniform; a failed step keeps the arithmetic finite and the barriers in
+// step, and the tile is discarded).
 __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, Misc* misc,
-                                        int warp, int lane) {
+                                        int warp, int lane, unsigned long long* pp) {
   const int lr = lane >> 2, lc = lane & 3;
+  // optional per-phase cycle counters (diagnostics; pp = this CTA's counters or null)
+  long long tprev = pp ? clock64() : 0;
+  auto lap = [&](int k) {
+    if (pp) {
+      const long long now = clock64();
+      if (lane == 0) atomicAdd(pp + k, (unsigned long long)(now - tprev));
+      tprev = now;
+    }
+  };
   double acc[2][16][2];
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
@@ -468,12 +486,15 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       acc[mi][ni][0] = v.x;
       acc[mi][ni][1] = v.y;
     }
-  double* Dblk = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [16][16]
-  double* P = Dblk + 256;                                                     // [128][16]
-  double* Stw = P + TILE * 16 + warp * (16 * kStageLd);                       // per warp
+  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
+  double* Pbuf = Dbuf + 2 * 256;                                              // [2][128][16]
+  double* Stw = Pbuf + 2 * TILE * 16 + warp * (16 * kStageLd);                // per warp
   for (int kb = 0; kb < 8; ++kb) {
     const int o = 16 * kb;
-    if (warp == kb) {
+    double* Dblk = Dbuf + (kb & 1) * 256;
+    double* P = Pbuf + (kb & 1) * (TILE * 16);
+    const int bd = 2 + (kb & 1), bp = 4 + (kb & 1);
+    if (warp == kb) {  // factor the pivot block, release it, done with this warp's rows
       stage_out(acc, Stw, lr, lc);
       __syncwarp();
       double xr[16];
@@ -486,54 +507,67 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       }
       __syncwarp();
       stage_in(acc, Stw, lr, lc);
-    }
-    consumer_sync();
-    if (misc->fail) return false;
-    if (warp > kb) {
-      stage_out(acc, Stw, lr, lc);
-      __syncwarp();
-      if (lane < 16) {
-        double xr[16];
-        load_row16(xr, Stw + lane * kStageLd);
-        solve_row16(xr, Dblk, rinvD + o);
-        store_row16(xr, Stw + lane * kStageLd);
-        const int r = 16 * warp + lane;
-#pragma unroll
-        for (int c = 0; c < 16; c += 2)
-          *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
-      }
-      __syncwarp();
-      stage_in(acc, Stw, lr, lc);
-    }
-    if (warp >= kb) {
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int nsub = 0; nsub < 2; ++nsub)
           *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
               make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+      if (kb < 7) named_bar_arrive(bd, 32 * (8 - kb));
+      lap(PR_P_PIV);
+      break;
     }
-    consumer_sync();  // the panel buffer is complete
-    if (warp > kb) {
-      double av[2][4];
-      window_afrags(acc, av, lane);
-      const int nlast = 2 * (warp - kb) + 1;  // the warp's own diagonal block
+    // warp > kb: the pivot block of step kb
+    named_bar_sync(bd, 32 * (8 - kb));
+    lap(PR_P_BDW);
+    stage_out(acc, Stw, lr, lc);
+    __syncwarp();
+    if (lane < 16) {
+      double xr[16];
+      load_row16(xr, Stw + lane * kStageLd);
+      solve_row16(xr, Dblk, rinvD + o);
+      store_row16(xr, Stw + lane * kStageLd);
+      const int r = 16 * warp + lane;
 #pragma unroll
-      for (int nb = 2; nb < 16; ++nb) {
-        if (nb <= nlast) {
-          const int prow = o + 8 * nb + lr;
+      for (int c = 0; c < 16; c += 2)
+        *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
+    }
+    __syncwarp();
+    stage_in(acc, Stw, lr, lc);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks) {
-            const double b = P[p_off(prow, 4 * ks + lc)];
-            dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
-            dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
-          }
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nsub = 0; nsub < 2; ++nsub)
+        *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
+            make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+    lap(PR_P_PANEL);
+    if (warp == kb + 1) {
+      named_bar_arrive(bp, 32 * (7 - kb));  // own panel rows are in P (the next warp's look-ahead
+                                            // needs only its own rows: nlast = 3 below)
+    } else {
+      named_bar_sync(bp, 32 * (7 - kb));    // every step-kb panel is in P
+    }
+    lap(PR_P_BPW);
+    double av[2][4];
+    window_afrags(acc, av, lane);
+    const int nlast = 2 * (warp - kb) + 1;  // the warp's own diagonal block
+#pragma unroll
+    for (int nb = 2; nb < 16; ++nb) {
+      if (nb <= nlast) {
+        const int prow = o + 8 * nb + lr;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const double b = P[p_off(prow, 4 * ks + lc)];
+          dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
+          dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
         }
       }
-      rotate_window(acc);
     }
+    rotate_window(acc);
+    lap(PR_P_UPD);
   }
-  return true;
+  consumer_sync();
+  return misc->fail == 0;
 }
 
 // DIAG-task tile products: the 136 (m-tile, n-tile) pairs of the 128 x 128 lower triangle
@@ -1017,9 +1051,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
         if (!skip) {
-          ok = diag_potrf(smem, C, rinvD, misc, warp, lane);
+          ok = diag_potrf(smem, C, rinvD, misc, warp, lane,
+                          a.prof ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr);
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
-          consumer_sync();
         }
         if (tid == 0) pr.lap(PR_POTRF);
         // L(j,j) -> HBM, then publish

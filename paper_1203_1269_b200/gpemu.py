@@ -616,7 +616,8 @@ class ProfileEvaluator:
 
     DAG_PHASES = ("ticket", "gemm", "acc_store", "potrf", "diag_store", "border", "off_wait",
                   "trsm", "off_store", "task_end", "prod_flags", "prod_empty", "n_diag", "n_off",
-                  "slabs", "total", "full_wait", "diag_full_wait", "diag_gemm")
+                  "slabs", "total", "full_wait", "diag_full_wait", "diag_gemm", "potrf_pivot",
+                  "potrf_bd_wait", "potrf_panel", "potrf_bp_wait", "potrf_update")
 
     def dag_profile(self, enable: bool = True, read: bool = False):
         """Diagnostics: arm / read the DAG engine's per-CTA phase cycle counters."""

@@ -11,7 +11,7 @@ import numpy as np
 # tickets are decoded here with the kernel's built-in column order: keep the list-schedule table off
 os.environ["GPEMU_TICKET_ORDER"] = "0"
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, ".")
 import paper_1203_1269_b200.gpemu as g  # noqa: E402
 
 n, d, B = (int(a) for a in sys.argv[1:4])
