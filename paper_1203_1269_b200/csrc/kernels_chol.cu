@@ -465,7 +465,7 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 // Finished blocks are written back into C. Reciprocal pivots -> rinvD[0..127]. Returns false
 // on a failed pivot (uniform; a failed step keeps the arithmetic finite and the barriers in
 // step, and the tile is discarded).
-__device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, Misc* misc,
+__device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, double* W, Misc* misc,
                                         int warp, int lane, unsigned long long* pp) {
   const int lr = lane >> 2, lc = lane & 3;
   // optional per-phase cycle counters (diagnostics; pp = this CTA's counters or null)
@@ -515,6 +515,35 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
               make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
       if (kb < 7) named_bar_arrive(bd, 32 * (8 - kb));
       lap(PR_P_PIV);
+      // The border rows W = [w_u; w_v] (2 x 128) ride along as two rows below the tile: the
+      // pivot warp, idle after its factorization, solves their block kb against D_kb (lanes
+      // 0/1) once warp kb-1 has applied block kb-1 to them (named barrier BB), then applies
+      // block kb to their trailing columns from the step-kb panels and hands over to warp
+      // kb+1. Each border element gets the same FMAs in the same order as a separate blocked
+      // substitution after the POTRF.
+      if (kb > 0) named_bar_sync(6 + (kb & 1), 64);
+      if (lane < 2) {
+        double xr[16];
+        load_row16(xr, W + lane * TILE + o);
+        solve_row16(xr, Dblk, rinvD + o);
+        store_row16(xr, W + lane * TILE + o);
+      }
+      __syncwarp();
+      if (kb < 7) {
+        named_bar_sync(bp, 32 * (8 - kb));  // the step-kb panels are in P
+        const int ncol = TILE - o - 16;
+        for (int q = lane; q < 2 * ncol; q += 32) {
+          const int r = q >= ncol ? 1 : 0;
+          const int l = o + 16 + q - r * ncol;
+          const double* x = W + r * TILE + o;
+          double sacc = W[r * TILE + l];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) sacc -= x[c] * P[p_off(l, c)];
+          W[r * TILE + l] = sacc;
+        }
+        __syncwarp();
+        named_bar_arrive(6 + ((kb + 1) & 1), 64);
+      }
       break;
     }
     // warp > kb: the pivot block of step kb
@@ -541,11 +570,12 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
         *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
             make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
     lap(PR_P_PANEL);
+    // BP(kb): warps kb+1..7 and the border-owning pivot warp kb
     if (warp == kb + 1) {
-      named_bar_arrive(bp, 32 * (7 - kb));  // own panel rows are in P (the next warp's look-ahead
+      named_bar_arrive(bp, 32 * (8 - kb));  // own panel rows are in P (the next warp's look-ahead
                                             // needs only its own rows: nlast = 3 below)
     } else {
-      named_bar_sync(bp, 32 * (7 - kb));    // every step-kb panel is in P
+      named_bar_sync(bp, 32 * (8 - kb));    // every step-kb panel is in P
     }
     lap(PR_P_BPW);
     double av[2][4];
@@ -1051,7 +1081,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
         if (!skip) {
-          ok = diag_potrf(smem, C, rinvD, misc, warp, lane,
+          ok = diag_potrf(smem, C, rinvD, W, misc, warp, lane,
                           a.prof ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr);
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
         }
@@ -1067,36 +1097,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           publish_flag(&flags[j * NT + j], epoch);
           pr.lap(PR_DIAG_STORE);
         }
-        // border solve: [u_j; v_j] = w L(j,j)^-T, blocked by 16 columns: lanes 0/1 of warp 0
-        // substitute the block in registers, then every consumer thread updates one (row,
-        // column) right of it with the block's 16 products. Each w element receives the same
-        // FMAs in the same column order as a column-by-column substitution.
+        // border rows [u_j; v_j] = w L(j,j)^-T: solved inside the POTRF (diag_potrf)
         if (ok) {
-          double* Dd = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);  // [8][16][16], idle ring tail
-          for (int q = tid; q < 2048; q += kConsumers) {
-            const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
-            Dd[q] = cc <= rr ? Cs(C, 16 * b8 + rr, 16 * b8 + cc) : 0.0;
-          }
-          consumer_sync();
-          for (int cb = 0; cb < 8; ++cb) {
-            const int o = 16 * cb;
-            if (warp == 0 && lane < 2) {
-              double xr[16];
-              load_row16(xr, W + lane * TILE + o);
-              solve_row16(xr, Dd + cb * 256, rinvD + o);
-              store_row16(xr, W + lane * TILE + o);
-            }
-            consumer_sync();
-            const int l = o + 16 + bc;
-            if (l < TILE) {
-              const double* x = W + brow * TILE + o;
-              double s = W[brow * TILE + l];
-#pragma unroll
-              for (int c = 0; c < 16; ++c) s -= x[c] * Cs(C, l, o + c);
-              W[brow * TILE + l] = s;
-            }
-            consumer_sync();
-          }
           if (tid < 2 * TILE) __stcg(bord + brow * Npad + j * TILE + bc, W[brow * TILE + bc]);
         }
         consumer_sync();
