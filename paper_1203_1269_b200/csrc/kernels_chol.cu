@@ -136,7 +136,7 @@ constexpr int kStageLd = 18;  // row stride (doubles) of the per-warp TRSM stagi
 // The OFF-task TRSM keeps its staging blocks and the packed diagonal blocks of L(j,j) above
 // the ring (L(j,j) itself occupies stages 0-1), so stage 2 stays free during the TRSM and
 // takes the next task's first slab.
-constexpr int kOffTrsmSt = kOffMisc + 128;                                  // [8 warps][16][kStageLd]
+constexpr int kOffTrsmSt = kOffMisc + 160;                                  // [8 warps][16][kStageLd]
 constexpr int kTriElems = 136;                                              // packed 16x16 lower
 constexpr int kOffTrsmD = kOffTrsmSt + kConsumerWarps * 16 * kStageLd * 8;  // [8][kTriElems]
 constexpr int kSmemBytes = kOffTrsmD + 8 * kTriElems * 8;
@@ -155,6 +155,8 @@ struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's 
   int pre_next;        // the previous task issued slab 0 of ticket `next` into stage 2
   int pre;             // this task's slab 0 is in stage 2 already
   int run;             // OFF task: the candidate was still unfailed at the TRSM start
+  int pcnt[4];         // DIAG: warp blocks of each L(j,j) slab stored (progressive publication)
+  int ljj_issued;      // OFF (chain-bound launches): L(j,j) slabs whose loads are issued
 };
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
@@ -466,8 +468,10 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 // on a failed pivot (uniform; a failed step keeps the arithmetic finite and the barriers in
 // step, and the tile is discarded).
 __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, double* W, Misc* misc,
-                                        int warp, int lane, unsigned long long* pp) {
+                                        int warp, int lane, unsigned long long* pp, double* gt, int* prog,
+                                        int pbase, double* bg, int npad, int* bprog) {
   const int lr = lane >> 2, lc = lane & 3;
+
   // optional per-phase cycle counters (diagnostics; pp = this CTA's counters or null)
   long long tprev = pp ? clock64() : 0;
   auto lap = [&](int k) {
@@ -486,7 +490,30 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       acc[mi][ni][0] = v.x;
       acc[mi][ni][1] = v.y;
     }
-  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
+  // Progressive publication: each finished 16x16 block also goes to HBM (gt), and when every
+  // block of an L(j,j) slab (column blocks 2s, 2s+1: 15 - 4s warp blocks) is stored, the last
+  // contributor releases the tile's flag as pbase + s + 1 (chain-bound OFF tasks start their
+  // TRSM on the first slab; others wait for pbase + 4).
+  auto store_block = [&](int kb) {
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int nsub = 0; nsub < 2; ++nsub) {
+        const int off = acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc);
+        *reinterpret_cast<double2*>(C + off) = make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+        if (gt) __stcg(reinterpret_cast<double2*>(gt + off), make_double2(acc[mi][nsub][0], acc[mi][nsub][1]));
+      }
+    if (!gt) return;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      const int sl = kb >> 1;
+      if (atomicAdd(&misc->pcnt[sl], 1) == 14 - 4 * sl) {
+        fence_proxy_async_global();
+        st_release_gpu(prog, pbase + sl + 1);
+      }
+    }
+  };  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
   double* Pbuf = Dbuf + 2 * 256;                                              // [2][128][16]
   double* Stw = Pbuf + 2 * TILE * 16 + warp * (16 * kStageLd);                // per warp
   for (int kb = 0; kb < 8; ++kb) {
@@ -507,13 +534,8 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       }
       __syncwarp();
       stage_in(acc, Stw, lr, lc);
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int nsub = 0; nsub < 2; ++nsub)
-          *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
-              make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
       if (kb < 7) named_bar_arrive(bd, 32 * (8 - kb));
+      store_block(kb);
       lap(PR_P_PIV);
       // The border rows W = [w_u; w_v] (2 x 128) ride along as two rows below the tile: the
       // pivot warp, idle after its factorization, solves their block kb against D_kb (lanes
@@ -529,6 +551,15 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
         store_row16(xr, W + lane * TILE + o);
       }
       __syncwarp();
+      // block kb of [u_j; v_j] is final: to HBM; after the odd block of a 32-column slab the
+      // slab is released (the even block's warp handed over through BB before this one began)
+      __stcg(bg + (lane >> 4) * npad + o + (lane & 15), W[(lane >> 4) * TILE + o + (lane & 15)]);
+      __syncwarp();
+      if ((kb & 1) && lane == 0) {
+        __threadfence();
+        fence_proxy_async_global();
+        st_release_gpu(bprog, pbase + (kb >> 1) + 1);
+      }
       if (kb < 7) {
         named_bar_sync(bp, 32 * (8 - kb));  // the step-kb panels are in P
         const int ncol = TILE - o - 16;
@@ -563,12 +594,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     }
     __syncwarp();
     stage_in(acc, Stw, lr, lc);
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int nsub = 0; nsub < 2; ++nsub)
-        *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
-            make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+    store_block(kb);
     lap(PR_P_PANEL);
     // BP(kb): warps kb+1..7 and the border-owning pivot warp kb
     if (warp == kb + 1) {
@@ -651,8 +677,8 @@ template <bool kProgress>
 __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kOffBar);
-  uint64_t* ljj_bar = full + kStages;  // L(j,j) bulk load for the OFF-task TRSM
-  int* stage_cnt = reinterpret_cast<int*>(ljj_bar + 1);  // warps done with each stage
+  uint64_t* ljj_bar = full + kStages;  // [4] L(j,j) loads for the OFF-task TRSM (one per slab)
+  int* stage_cnt = reinterpret_cast<int*>(ljj_bar + 4);  // warps done with each stage
   double* C = reinterpret_cast<double*>(smem + kOffC);
   double* W = reinterpret_cast<double*>(smem + kOffW);
   double* rinvD = reinterpret_cast<double*>(smem + kOffRinvD);
@@ -675,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       mbar_init(&full[s], 1);
       stage_cnt[s] = 0;
     }
-    mbar_init(ljj_bar, 1);
+    for (int s = 0; s < 4; ++s) mbar_init(&ljj_bar[s], 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -834,7 +860,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           } else {
             f = diag ? &flags[NT * NT + K] : &flags[I * NT + K];
           }
-          if (f && ld_acquire_gpu(f) == epoch) atomicOr(&misc->ready[8 * part + (K >> 5)], 1u << (K & 31));
+          // (border flags are progressive: 4 epoch + slabs released, complete at 4 epoch + 4)
+          const int want = (diag && part == 1) ? 4 * epoch + 4 : epoch;
+          if (f && (diag && part == 1 ? ld_acquire_gpu(f) >= want : ld_acquire_gpu(f) == want))
+            atomicOr(&misc->ready[8 * part + (K >> 5)], 1u << (K & 31));
         }
         __syncwarp();
       }
@@ -851,8 +880,8 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             wait_flag(&a.ext_flags[(size_t)It * NT + K], epoch, a.error);
           } else {
             if (!(slab_progress && diag && K == j - 1)) wait_flag(&flags[j * NT + K], epoch, a.error);
-            if (diag) {
-              wait_flag(&flags[NT * NT + K], epoch, a.error);
+            if (diag) {  // border rows of column K (progressive: 4 epoch + slabs done)
+              if (!(slab_progress && K == j - 1)) wait_flag_geq(&flags[NT * NT + K], 4 * epoch + 4, a.error);
             } else {
               wait_flag(&flags[I * NT + K], epoch, a.error);
             }
@@ -866,6 +895,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           // the sub-diagonal tile L(j, j-1) is consumed slab by slab as its OFF task's TRSM
           // finishes them: progress word flags[(j-1)*NT + j] = 4*epoch + slabs done
           wait_flag_geq(&flags[(j - 1) * NT + j], 4 * epoch + sq + 1, a.error);
+          wait_flag_geq(&flags[NT * NT + K], 4 * epoch + sq + 1, a.error);  // and its border segment
           fence_proxy_async_global();
         }
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
@@ -1001,6 +1031,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // first (every warp waits for it), then the take-ahead of the next ticket -- several
       // dependent L2 round trips (ticket, order table, slot, status, flags) that now overlap
       // the L(j,j) transfer instead of preceding it.
+      auto issue_ljj = [&](int sl) {  // slab sl of L(j,j) -> stage ring bytes [32 KB sl, +32 KB)
+        fence_proxy_async_global();
+        mbar_arrive_expect_tx(&ljj_bar[sl], kSlabBytes);
+        bulk_g2s(smem + sl * kSlabBytes, fac + tile_index(j, j) * TILE_ELEMS + sl * SLAB_ELEMS, kSlabBytes,
+                 &ljj_bar[sl]);
+      };
       auto take_next = [&]() {
       if (take_ahead && misc->ticket < ntasks - 2 * (int)gridDim.x) {
         const int tn = atomicAdd(a.counter, 1);
@@ -1019,7 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             const int* fln = a.flags + (size_t)sn * fstride;
             const bool dn = In == jn;
             if (ld_acquire_gpu(&fln[jn * NT]) == epoch &&
-                ld_acquire_gpu(dn ? &fln[NT * NT] : &fln[In * NT]) == epoch) {
+                (dn ? ld_acquire_gpu(&fln[NT * NT]) >= 4 * epoch + 4 : ld_acquire_gpu(&fln[In * NT]) == epoch)) {
               fence_proxy_async_global();
               fence_proxy_async_shared();  // generic-proxy reads of stage 2 before the TMA write
               const double* facn = a.factors + (size_t)sn * a.slot_stride;
@@ -1043,13 +1079,23 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       if (tid == 0) {
         if (!diag && !skip) {
           misc->run = ext || *((volatile int*)&a.status[slot]) == 0;
-          if (!ext) wait_flag(&flags[j * NT + j], epoch, a.error);
-          fence_proxy_async_global();
-          mbar_arrive_expect_tx(ljj_bar, TILE_ELEMS * 8);
-          const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
+          if constexpr (kProgress) {  // slab 0 now (blocking), later slabs when already published
+            if (!ext) wait_flag_geq(&flags[j * NT + j], 4 * epoch + 1, a.error);
+            int is = 0;
+            do {
+              issue_ljj(is);
+              ++is;
+            } while (is < SLABS_PER_TILE && (ext || ld_acquire_gpu(&flags[j * NT + j]) >= 4 * epoch + is + 1));
+            misc->ljj_issued = is;
+          } else {
+            if (!ext) wait_flag_geq(&flags[j * NT + j], 4 * epoch + 4, a.error);
+            fence_proxy_async_global();
+            mbar_arrive_expect_tx(&ljj_bar[0], TILE_ELEMS * 8);
+            const double* Ljj = fac + tile_index(j, j) * TILE_ELEMS;
 #pragma unroll
-          for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
-            bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, ljj_bar);
+            for (int s4 = 0; s4 < SLABS_PER_TILE; ++s4)
+              bulk_g2s(smem + s4 * kSlabBytes, Ljj + s4 * SLAB_ELEMS, kSlabBytes, &ljj_bar[0]);
+          }
         }
         take_next();
       }
@@ -1077,33 +1123,40 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           for (int nn = 0; nn < 2; ++nn)
             *reinterpret_cast<double2*>(W + lr * TILE + 16 * warp + 8 * nn + 2 * lc) = make_double2(wb[nn][0], wb[nn][1]);
         }
+        if (tid == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) misc->pcnt[q] = 0;
+        }
         consumer_sync();
         if (tid == 0) pr.lap(PR_ACC_STORE);
         bool ok = !skip;
         if (!skip) {
           ok = diag_potrf(smem, C, rinvD, W, misc, warp, lane,
-                          a.prof ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr);
+                          a.prof ? a.prof + (size_t)blockIdx.x * PR_COUNT : nullptr, kProgress ? gtile : nullptr,
+                          &flags[j * NT + j], 4 * epoch, bord + j * TILE, Npad, &flags[NT * NT + j]);
           if (!ok && tid == 0) atomicExch(&a.status[slot], 1);  // GPEMU_SLOT_NOT_PD
         }
         if (tid == 0) pr.lap(PR_POTRF);
-        // L(j,j) -> HBM, then publish
-        if (ok) {
-          for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
-            __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
+        // Chain-bound launches stored L(j,j) block by block inside the POTRF (progressive release);
+        // throughput-bound ones store it now (per-block fences cost 0.1-1% there). Then the final
+        // release (also for skipped tasks, whose waiters must not block).
+        if constexpr (!kProgress) {
+          if (ok) {
+            for (int e = 2 * tid; e < TILE_ELEMS; e += 2 * kConsumers)
+              __stcg(reinterpret_cast<double2*>(gtile + e), *reinterpret_cast<const double2*>(C + e));
+          }
+          consumer_sync();
         }
-        consumer_sync();
         stamp(2);
         if (tid == 0) {
-          publish_flag(&flags[j * NT + j], epoch);
+          publish_flag(&flags[j * NT + j], 4 * epoch + 4);
           pr.lap(PR_DIAG_STORE);
         }
         // border rows [u_j; v_j] = w L(j,j)^-T: solved inside the POTRF (diag_potrf)
-        if (ok) {
-          if (tid < 2 * TILE) __stcg(bord + brow * Npad + j * TILE + bc, W[brow * TILE + bc]);
-        }
-        consumer_sync();
+        // (stored and released slab by slab inside the POTRF; the final release covers skipped
+        // tasks)
         if (tid == 0) {
-          publish_flag(&flags[NT * NT + j], epoch);
+          publish_flag(&flags[NT * NT + j], 4 * epoch + 4);
           pr.lap(PR_BORDER);
         }
       } else {
@@ -1113,12 +1166,19 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         // each warp then solves its own 16 rows in registers, 16 columns at a time:
         // (a) in-block substitution (quad shuffles), (b) DMMA update of the columns to
         // the right, (c) store the finished block, (d) rotate the accumulator window.
-        if (!skip) mbar_wait(ljj_bar, misc->ljj_phase & 1);  // issued by thread 0 at mainloop end
+        if (!skip) mbar_wait(&ljj_bar[0], misc->ljj_phase & 1);  // issued by thread 0 at mainloop end
         if (tid == 0) pr.lap(PR_OFF_WAIT);
         // uniform across the CTA (the TRSM below has CTA barriers): thread 0 read the status
         // once before the L(j,j) load, and the load's mbarrier publishes it (a later DIAG of the
         // same candidate may fail meanwhile: the TRSM then only does wasted work)
         const bool run = !skip && misc->run != 0;
+        if constexpr (kProgress) {
+          if (!skip && !run) {  // keep every slab barrier's phase in step: load (and drop) the rest
+            if (tid == 0)
+              for (int sl = misc->ljj_issued; sl < SLABS_PER_TILE; ++sl) issue_ljj(sl);
+            for (int sl = 1; sl < SLABS_PER_TILE; ++sl) mbar_wait(&ljj_bar[sl], misc->ljj_phase & 1);
+          }
+        }
         if (run) {
           const double* Ls = reinterpret_cast<const double*>(smem);  // L(j,j), tile layout
           // 1 / L_cc once per task; the in-block substitution forms a / L_cc as
@@ -1128,12 +1188,14 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           double* rinv = W;
           double* Dp = reinterpret_cast<double*>(smem + kOffTrsmD);              // [8][kTriElems]
           double* St = reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * (16 * kStageLd);
-          if (tid < TILE) rinv[tid] = 1.0 / Ls[elem_off(tid, tid)];
-          for (int q = tid; q < 2048; q += kConsumers) {
-            const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
-            if (cc <= rr) Dp[b8 * kTriElems + rr * (rr + 1) / 2 + cc] = Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)];
+          if constexpr (!kProgress) {
+            if (tid < TILE) rinv[tid] = 1.0 / Ls[elem_off(tid, tid)];
+            for (int q = tid; q < 2048; q += kConsumers) {
+              const int b8 = q >> 8, rr = (q >> 4) & 15, cc = q & 15;
+              if (cc <= rr) Dp[b8 * kTriElems + rr * (rr + 1) / 2 + cc] = Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)];
+            }
+            consumer_sync();
           }
-          consumer_sync();
           // Fully unrolled over the eight 16-column blocks: window n-tiles w = 2cb, 2cb+1 are
           // compile-time register indices (no rotation), and every L(j,j) operand address is a
           // per-lane base plus an immediate, so the DMMAs of independent column blocks
@@ -1142,6 +1204,30 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
 #pragma unroll
           for (int cb = 0; cb < 8; ++cb) {
             const int o = 16 * cb, w = 2 * cb;
+            if constexpr (kProgress) {
+              // L(j,j) slab cb/2: its load (issued once the DIAG task published it), then the
+              // reciprocal pivots and packed diagonal blocks of its two column blocks
+              if ((cb & 1) == 0) {
+                const int sl = cb >> 1;
+                if (tid == 0) {
+                  int is = misc->ljj_issued;
+                  for (; is <= sl; ++is) {
+                    wait_flag_geq(&flags[j * NT + j], 4 * epoch + is + 1, a.error);
+                    issue_ljj(is);
+                  }
+                  for (; is < SLABS_PER_TILE && ld_acquire_gpu(&flags[j * NT + j]) >= 4 * epoch + is + 1; ++is)
+                    issue_ljj(is);
+                  misc->ljj_issued = is;
+                }
+                if (sl > 0) mbar_wait(&ljj_bar[sl], misc->ljj_phase & 1);
+                if (tid < 32) rinv[32 * sl + tid] = 1.0 / Ls[elem_off(32 * sl + tid, 32 * sl + tid)];
+                for (int q = tid; q < 512; q += kConsumers) {
+                  const int b8 = 2 * sl + (q >> 8), rr = (q >> 4) & 15, cc = q & 15;
+                  if (cc <= rr) Dp[b8 * kTriElems + rr * (rr + 1) / 2 + cc] = Ls[elem_off(16 * b8 + rr, 16 * b8 + cc)];
+                }
+                consumer_sync();
+              }
+            }
             // (a) columns o..o+15 (acc[mi][w..w+1]): through the warp's staging block so
             // lane r < 16 owns row r and substitutes in registers
             stage_out_at(acc, w, St, lr, lc);
