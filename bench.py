@@ -58,8 +58,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fit", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-single", action="store_true",
-                    help="skip the informational single-precision (FP32 engine) rate")
+    ap.add_argument("--single", action="store_true",
+                    help="also time the FP32 engine on the same batches (informational; not a GA-batch "
+                         "path: most GA candidates climb the float jitter ladder, see DESIGN K2s)")
+    ap.add_argument("--no-single", action="store_true", help="(default; kept for old command lines)")
     ap.add_argument("--cpu-sample", type=int, default=0, help="evals in the CPU sample (0: auto)")
     ap.add_argument("--no-weak", action="store_true", help="N > 1: skip the weak-scaling leg")
     ap.add_argument("--no-latency", action="store_true",
@@ -525,7 +527,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_latency:
         line["latency"] = latency_leg(args, r)
     # ---- informational: the same batches on the single-precision engine (Precision::kSingle) ----
-    if rank == 0 and world == 1 and not args.no_single:
+    if rank == 0 and world == 1 and args.single and not args.no_single:
         import paper_1203_1269_b200.gpemu as g
         evs = g.ProfileEvaluator(r["data"], args.p, args.nugget, r["be"], max_batch=B,
                                  precision="single")
