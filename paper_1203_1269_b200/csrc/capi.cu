@@ -422,7 +422,10 @@ void release(H* h) {
 
 constexpr int kTraceTasks = 65536;  // DAG timeline capacity (diagnostics)
 constexpr double kOrderQuantum = 0.0;  // us; ticket_order priority quantum (0: exact bottom level)
-constexpr double kOrderTail = 0.7;     // ticket_order: exact priority only below this fraction of the longest path
+// ticket_order: exact priority only below this fraction of the longest path (large tile counts:
+// the L2-friendly setting; small ones: the faster one)
+constexpr double kOrderTailLarge = 0.4;  // NT >= 24
+constexpr double kOrderTailSmall = 0.7;
 
 // Ticket order for a large launch (B candidates x NT(NT+1)/2 tile tasks): a list schedule on
 // P processors with estimated task times (OFF(I,j): ~4 + 18.5 j + 20 us, DIAG(j): ~8 + 18.6 j
@@ -475,7 +478,10 @@ std::vector<int> ticket_order(int B, int NT, int P) {
   // everywhere 85.4 GB, +0.3%; the built-in column order 79.3 GB, +1.3%
   // (tools/order_quantum_sweep.sh). Round 2, with the operand-flag snapshot (GPEMU_ORDER_TAIL
   // sweep, alternating runs): 0.7 is the best of {0, 0.2, 0.4, 0.55, 0.7, 0.85} over C3
-  // (73.26 ms vs 73.31 at 0.4), C2 (7.39 vs 7.53) and a 100-candidate n=1024 batch (2.09 vs 2.15). GPEMU_ORDER_Q quantises the exact part (microseconds).
+  // (73.26 ms vs 73.31 at 0.4), C2 (7.39 vs 7.53) and a 100-candidate n=1024 batch (2.09 vs 2.15).
+  // Later in the round, at C3 the time no longer depends on it (71.23 ms at 0.4, 71.22 at 0.7)
+  // while the DRAM reads do (101.7 GB at 0.4, 134.2 GB at 0.7; tools/order_tail_sweep.sh), so
+  // NT >= 24 (n > 2944) uses 0.4 and smaller designs 0.7. GPEMU_ORDER_Q quantises the exact part (microseconds).
   const char* qenv = std::getenv("GPEMU_ORDER_Q");
   const double quantum = qenv ? std::atof(qenv) : kOrderQuantum;
   struct Ready {
@@ -489,7 +495,7 @@ std::vector<int> ticket_order(int B, int NT, int P) {
     }
   };
   const char* tenv = std::getenv("GPEMU_ORDER_TAIL");
-  const double tail_frac = tenv ? std::atof(tenv) : kOrderTail;
+  const double tail_frac = tenv ? std::atof(tenv) : (NT >= 24 ? kOrderTailLarge : kOrderTailSmall);
   double max_bl = 0.0;
   for (int t = 0; t < T; ++t) max_bl = std::max(max_bl, bl[t]);
   auto mk = [&](int b, int t) {
