@@ -423,7 +423,7 @@ __device__ __forceinline__ void pivot_root(double s, double& d, double& r) {
 // element gets the same operations in the same order as a column-by-column right-looking
 // loop; the upper triangle of xr is left undefined (never read). Pivot reciprocals ->
 // rinv[0..15]. Returns false (uniform) on a failed pivot (backend.hpp:238).
-__device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int lane) {
+__device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int lane, double* qs) {
   double d, r;
   double s = __shfl_sync(0xffffffffu, xr[0], 0);
   bool ok = s > 0.0;  // uniform: every lane sees the same pivots
@@ -440,8 +440,13 @@ __device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int 
       if (!ok) sn = 1.0;
       pivot_root(sn, d, r);
     }
+    // column c's quotients to every lane through shared memory (one STS per lane, broadcast
+    // LDS): 15 - c double shuffles per column made the block 1.65x slower
+    // (tools/microbench/potrf16.cu: 7.6k -> 4.6k cycles); double-buffered by column parity
+    if (lane < 16) qs[16 * (c & 1) + lane] = q;
+    __syncwarp();
 #pragma unroll
-    for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] = fma(-q, __shfl_sync(0xffffffffu, q, c2), xr[c2]);
+    for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] = fma(-q, qs[16 * (c & 1) + c2], xr[c2]);
   }
   return ok;
 }
@@ -526,7 +531,9 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       __syncwarp();
       double xr[16];
       if (lane < 16) load_row16(xr, Stw + lane * kStageLd);
-      const bool okw = potrf_row16(xr, rinvD + o, lane);
+      // quotient broadcast buffer: the OFF-TRSM staging area, idle during DIAG tasks
+      const bool okw = potrf_row16(xr, rinvD + o, lane,
+                                   reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * 32);
       if (!okw && lane == 0) misc->fail = 1;
       if (lane < 16) {
         store_row16(xr, Stw + lane * kStageLd);
