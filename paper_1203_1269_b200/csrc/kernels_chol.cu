@@ -470,8 +470,8 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 // operations in the same order as without the look-ahead. Pivot blocks and panels are double-
 // buffered by step parity (the barriers keep any warp within one step of its readers).
 // Finished blocks are written back into C. Reciprocal pivots -> rinvD[0..127]. Returns false
-// on a failed pivot (uniform; a failed step keeps the arithmetic finite and the barriers in
-// step, and the tile is discarded).
+// on a failed pivot (uniform): the factorization stops at that step with the barriers balanced,
+// and the tile is discarded.
 __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* rinvD, double* W, Misc* misc,
                                         int warp, int lane, unsigned long long* pp, double* gt, int* prog,
                                         int pbase, double* bg, int npad, int* bprog) {
@@ -551,6 +551,10 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       // kb+1. Each border element gets the same FMAs in the same order as a separate blocked
       // substitution after the POTRF.
       if (kb > 0) named_bar_sync(6 + (kb & 1), 64);
+      // A failed pivot ends the factorization here (as the reference's factor attempt does): the
+      // warps below see misc->fail after BD(kb) and stop too; BB's pending arrival is consumed
+      // above and BP / BB(kb+1) are not entered by anyone, so the barriers stay balanced.
+      if (!okw) break;
       if (lane < 2) {
         double xr[16];
         load_row16(xr, W + lane * TILE + o);
@@ -587,6 +591,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     // warp > kb: the pivot block of step kb
     named_bar_sync(bd, 32 * (8 - kb));
     lap(PR_P_BDW);
+    if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
     stage_out(acc, Stw, lr, lc);
     __syncwarp();
     if (lane < 16) {

@@ -702,3 +702,27 @@ def test_speculative_ladder_rung_bitwise(g, ctx, monkeypatch):
     assert np.array_equal(L_spec, L_plain)
     monkeypatch.delenv("GPEMU_SPEC_LADDER")
     ev.close()
+
+
+def test_ladder_invariance_across_kernel_instantiations(g, ctx):
+    """Candidates that fail a pivot partway through the factorization (squared exponential at
+    n=1000: most thetas climb the jitter ladder) in chain-bound launches -- slab-wise
+    release of L(j,j) and of the border rows, the TRSM's per-slab loads and its drop path for
+    a candidate that failed meanwhile -- against the same thetas inside a 100-candidate
+    throughput launch: bitwise the same records, jitter steps included."""
+    rng = np.random.default_rng(2024)
+    n, d = 1000, 3
+    X = rng.random((n, d))
+    y = np.sin(3 * X).sum(1)
+    th = 10 ** rng.uniform(-4.0, 1.5, size=(100, d))  # p = 2: most climb to 1e-8, a few do not
+    ev = g.ProfileEvaluator(g.new_dataset(X, y), 2.0, 0.0, g.Backend(ctx), max_batch=100)
+    big = ev.eval_batch(th)
+    assert np.any(big["jitter"] > 0) and np.any(big["jitter"] == 0), "the batch should mix ladder steps"
+    for lo in (0, 8, 56, 92):
+        small = ev.eval_batch(th[lo:lo + 8])
+        for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+            assert np.array_equal(big[k][lo:lo + 8], small[k]), (k, lo)
+    for i in np.nonzero(big["jitter"] > 0)[0][:3]:
+        one = ev.eval_batch(th[i:i + 1])
+        assert one["jitter"][0] == big["jitter"][i] and one["neg2"][0] == big["neg2"][i]
+    ev.close()
