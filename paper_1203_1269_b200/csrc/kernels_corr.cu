@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     double nugget, int NT, const int* __restrict__ slots, int nslots,
     const double* __restrict__ jitter, double* __restrict__ factors, size_t slot_stride,
     int* __restrict__ status) {
-  __shared__ double th[kAsmSlotChunk * MAXD];
+  __shared__ __align__(16) double th[kAsmSlotChunk * MAXD];  // [k][slot]: slot pairs load as double2
   __shared__ int sl[kAsmSlotChunk];
   __shared__ long long soff[kAsmSlotChunk];
   const int tile = blockIdx.x;
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
     // to the same address), so the kSlotILP groups below need no per-slot guard.
     for (int q = threadIdx.x; q < kAsmSlotChunk * MAXD; q += blockDim.x) {
       const int si = q / MAXD, k = q - si * MAXD;
-      th[q] = k < d ? theta[(size_t)slots[c0 + min(si, cn - 1)] * d + k] : 0.0;
+      th[k * kAsmSlotChunk + si] = k < d ? theta[(size_t)slots[c0 + min(si, cn - 1)] * d + k] : 0.0;
     }
     for (int q = threadIdx.x; q < kAsmSlotChunk; q += blockDim.x) {
       const int slot = slots[c0 + min(q, cn - 1)];
@@ -132,7 +132,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
 #pragma unroll
-          for (int q = 0; q < kSlotILP; ++q) s[q] = fma(th[(s0 + q) * MAXD + k], t[k], s[q]);
+          for (int q = 0; q < kSlotILP; q += 2) {
+            const double2 tq = *reinterpret_cast<const double2*>(th + k * kAsmSlotChunk + s0 + q);
+            s[q] = fma(tq.x, t[k], s[q]);
+            s[q + 1] = fma(tq.y, t[k], s[q + 1]);
+          }
         }
 #pragma unroll
         for (int q = 0; q < kSlotILP; ++q) v[q] = exp_neg(s[q]);
