@@ -143,7 +143,9 @@ __global__ void __launch_bounds__(256) assemble_kernel(
 #pragma unroll
         for (int q = 0; q < kSlotILP; ++q) {
           dst[soff[s0 + q]] = v[q];
-          if (!isfinite(v[q]) || isnan(s[q])) status[sl[s0 + q]] = 2;  // GPEMU_SLOT_NONFINITE (correlation.hpp:58-61)
+          // GPEMU_SLOT_NONFINITE (correlation.hpp:58-61): s >= 0 for validated inputs, so exp(-s)
+          // is non-finite exactly when s is NaN (exp_neg maps NaN to 0)
+          if (s[q] != s[q]) status[sl[s0 + q]] = 2;
         }
       }
     }
