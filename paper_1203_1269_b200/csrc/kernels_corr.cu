@@ -74,12 +74,12 @@ constexpr int kSlotILP = 8;
 // candidate of the batch; kSlotILP candidates are processed together, branch-free (exp_neg,
 // stores predicated), so their k-sums and exps interleave. MAXD is a compile-time bound on d
 // (dispatch below), so the k loop is fully unrolled with no dead iterations.
-template <int MAXD>
+template <int MAXD, bool kSplit>
 __global__ void __launch_bounds__(256) assemble_kernel(
     const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
     double nugget, int NT, const int* __restrict__ slots, int nslots,
     const double* __restrict__ jitter, double* __restrict__ factors, size_t slot_stride,
-    int* __restrict__ status) {
+    int* __restrict__ status, int chunk) {
   __shared__ __align__(16) double th[kAsmSlotChunk * MAXD];  // [k][slot]: slot pairs load as double2
   __shared__ int sl[kAsmSlotChunk];
   __shared__ long long soff[kAsmSlotChunk];
@@ -92,8 +92,11 @@ __global__ void __launch_bounds__(256) assemble_kernel(
   const double diag_base = __dadd_rn(1.0, nugget);  // correlation.hpp:193
   double* const fbase = factors + (size_t)tile * TILE_ELEMS;
 
-  for (int c0 = 0; c0 < nslots; c0 += kAsmSlotChunk) {
-    const int cn = min(kAsmSlotChunk, nslots - c0);
+  // candidate chunks of `chunk` (<= kAsmSlotChunk) slots, spread over blockIdx.z on small designs
+  // (kSplit: a separate instantiation, so the large-design code keeps its register allocation)
+  const int cstep = kSplit ? chunk : kAsmSlotChunk;
+  for (int c0 = kSplit ? blockIdx.z * chunk : 0; c0 < nslots; c0 += kSplit ? gridDim.z * chunk : kAsmSlotChunk) {
+    const int cn = min(cstep, nslots - c0);
     __syncthreads();
     // Entries past cn replicate the last live slot (same theta -> the same value rewritten
     // to the same address), so the kSlotILP groups below need no per-slot guard.
@@ -208,9 +211,13 @@ __global__ void __launch_bounds__(256) assemble_generic_kernel(
 template <int MAXD>
 static void launch_asm(dim3 grid, cudaStream_t s, const double* table, const double* theta, int n,
                        int d, double nugget, int NT, const int* slots, int nslots,
-                       const double* jitter, double* factors, size_t slot_stride, int* status) {
-  assemble_kernel<MAXD><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
-                                             factors, slot_stride, status);
+                       const double* jitter, double* factors, size_t slot_stride, int* status, int chunk) {
+  if (grid.z > 1)
+    assemble_kernel<MAXD, true><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                                     factors, slot_stride, status, chunk);
+  else
+    assemble_kernel<MAXD, false><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                                      factors, slot_stride, status, chunk);
 }
 
 void launch_assemble(const double* table, const double* theta, const double* y, int n, int d,
@@ -224,10 +231,19 @@ void launch_assemble(const double* table, const double* theta, const double* y, 
   // at most one element per thread per slot chunk (TILE_ELEMS / 256 = 64)
   const int tiles = num_tiles(NT);
   const int gy = std::min(64, std::max(8, (8 * num_sms + tiles - 1) / tiles));
-  const dim3 grid(tiles, gy);
+  // Small designs (n=200: 3 tiles, 192 blocks) are too few blocks to keep the R stores in flight:
+  // split the candidates over blockIdx.z as well (each block then reloads its elements' table
+  // values, which large designs avoid). C1: 33 -> ~10 us per batch.
+  int chunk = kAsmSlotChunk, gz = 1;
+  if (tiles * gy < 4 * num_sms && nslots > 8) {
+    gz = std::min((nslots + 7) / 8, (4 * num_sms + tiles * gy - 1) / (tiles * gy));
+    chunk = std::min(kAsmSlotChunk, ((nslots + gz - 1) / gz + 7) / 8 * 8);
+    gz = (nslots + chunk - 1) / chunk;
+  }
+  const dim3 grid(tiles, gy, gz);
   // theta entries beyond d are zero in shared memory, so a looser bound is only slower
 #define GPEMU_ASM(D) \
-  launch_asm<D>(grid, s, table, theta, n, d, nugget, NT, slots, nslots, jitter, factors, slot_stride, status)
+  launch_asm<D>(grid, s, table, theta, n, d, nugget, NT, slots, nslots, jitter, factors, slot_stride, status, chunk)
   if (d <= 1) GPEMU_ASM(1);
   else if (d <= 2) GPEMU_ASM(2);
   else if (d <= 3) GPEMU_ASM(3);
@@ -241,7 +257,7 @@ void launch_assemble(const double* table, const double* theta, const double* y, 
   else if (d <= 24) GPEMU_ASM(24);
   else if (d <= 32) GPEMU_ASM(32);
   else
-    assemble_generic_kernel<<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+    assemble_generic_kernel<<<dim3(grid.x, grid.y), 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
                                                  factors, slot_stride, status);
 #undef GPEMU_ASM
 }
