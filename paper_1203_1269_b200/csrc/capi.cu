@@ -2275,7 +2275,7 @@ int gpemu_maximin_lhd(gpemu_ctx* ctx, size_t n, size_t d, uint64_t seed, size_t 
   gpemu_dev::MaximinLaunch L{dX.p, (int)n, (int)d, (int)exchange_budget, dD.p, r0.p, r1.p, dra.p, drb.p, fl.p,
                              red.p, red.p + 8, res.p};
   ck(gpemu_dev::launch_maximin(L, ctx->num_sms, s), "maximin launch");
-  ctx->launches += 2;
+  ctx->launches += 3;
   double hres[2];
   ck(cudaMemcpyAsync(x_out, dX.p, n * d * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H design");
   ck(cudaMemcpyAsync(hres, res.p, sizeof(hres), cudaMemcpyDeviceToHost, s), "D2H result");

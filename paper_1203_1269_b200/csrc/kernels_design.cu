@@ -29,6 +29,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -74,8 +75,14 @@ __device__ __forceinline__ double block_min(double v, double* red) {
   return v;
 }
 
+__global__ void fill_u64_kernel(unsigned long long* __restrict__ p, int n, unsigned long long v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) p[i] = v;
+}
+
 // MinDistanceTracker constructor (experiment.hpp:64-75): every row's minimum distance, and the
-// global minimum into *gmin. One thread per row; column rows are staged in shared memory.
+// global minimum into *gmin. One thread per row and a column range per blockIdx.y (rows and
+// column ranges spread over the SMs; rmin pre-filled with +inf, combined by atomicMin); column
+// rows are staged in shared memory.
 __global__ void __launch_bounds__(256) maximin_init_kernel(const double* __restrict__ x, int n, int d,
                                                           unsigned long long* __restrict__ rmin,
                                                           unsigned long long* __restrict__ gmin) {
@@ -83,9 +90,11 @@ __global__ void __launch_bounds__(256) maximin_init_kernel(const double* __restr
   __shared__ double red[32];
   const int tr = max(1, min(64, 6144 / d));
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  const int per = (n + gridDim.y - 1) / gridDim.y;
+  const int cbeg = blockIdx.y * per, cend = min(n, cbeg + per);
   double m = __longlong_as_double(kInfBits);
-  for (int c0 = 0; c0 < n; c0 += tr) {
-    const int rows = min(tr, n - c0);
+  for (int c0 = cbeg; c0 < cend; c0 += tr) {
+    const int rows = min(tr, cend - c0);
     __syncthreads();
     for (int e = threadIdx.x; e < rows * d; e += blockDim.x) xs[e] = x[(size_t)c0 * d + e];
     __syncthreads();
@@ -97,7 +106,7 @@ __global__ void __launch_bounds__(256) maximin_init_kernel(const double* __restr
       }
     }
   }
-  if (r < n) rmin[r] = dbits(m);
+  if (r < n) atomicMin(&rmin[r], dbits(m));
   const double bm = block_min(r < n ? m : __longlong_as_double(kInfBits), red);
   if (threadIdx.x == 0) atomicMin(gmin, dbits(bm));
 }
@@ -242,7 +251,10 @@ cudaError_t launch_maximin(const MaximinLaunch& a, int num_sms, cudaStream_t s) 
     cudaError_t e = cudaFuncSetAttribute(maximin_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  maximin_init_kernel<<<(a.n + 255) / 256, 256, smem, s>>>(a.x, a.n, a.d, a.rmin0, a.init_min);
+  fill_u64_kernel<<<(a.n + 255) / 256, 256, 0, s>>>(a.rmin0, a.n, kInfBits);
+  const int gx = (a.n + 255) / 256;
+  const int gy = std::max(1, std::min(std::max(1, a.n / 256), (4 * num_sms + gx - 1) / gx));
+  maximin_init_kernel<<<dim3(gx, gy), 256, smem, s>>>(a.x, a.n, a.d, a.rmin0, a.init_min);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || a.budget == 0) return e;
   int per_sm = 0;
