@@ -2,7 +2,7 @@
 slab-0 prefetch, ladder relaunches): random designs and theta batches -- many candidates
 failing pivots at various columns -- evaluated (a) twice in a 100-candidate launch, (b) in
 8-candidate and single-candidate launches (the chain-bound instantiation), all of which must
-agree bitwise; plus the deadlock word. usage: python tools/stress_dag.py [seconds]"""
+agree bitwise; plus the deadlock word. usage: python tools/stress_dag.py [seconds] [n1,n2,...]"""
 import sys
 import time
 
@@ -12,13 +12,14 @@ sys.path.insert(0, ".")
 import paper_1203_1269_b200.gpemu as g  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300.0
+sizes = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [130, 257, 600, 1000, 1500, 2100]
 ctx = g.Context(0)
 be = g.Backend(ctx)
 rng = np.random.default_rng(12345)
 t_end = time.time() + budget
 cases = mism = 0
 while time.time() < t_end:
-    n = int(rng.choice([130, 257, 600, 1000, 1500, 2100]))
+    n = int(rng.choice(sizes))
     d = int(rng.integers(1, 7))
     p = float(rng.choice([1.0, 1.5, 1.95, 2.0]))
     X = rng.random((n, d))
