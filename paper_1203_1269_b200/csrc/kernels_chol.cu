@@ -855,9 +855,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // blocking wait). Published tiles are marked in misc->ready; their TMA loads are issued
       // without touching the flags again, the rest take the blocking wait. The refill of slab
       // 4 (K-tile 1) needs every warp past slab 1, so the bits are written by then (stage
-      // counter atomics after __threadfence_block order them). Short tasks (j < 8) keep the
-      // per-K-tile waits: their inputs are mostly unpublished at task start (n=1024: +2%).
-      if (warp == kConsumerWarps - 1 && j >= 8) {
+      // counter atomics after __threadfence_block order them). Every task with more than one
+      // K-tile takes the snapshot (thresholds of 4 and 8 K-tiles were 0.1-0.5% slower).
+      if (warp == kConsumerWarps - 1 && j >= 2) {
         const int kmax = j < 256 ? j : 256;
         if (lane < 16) misc->ready[lane] = 0u;  // [0, 8): first flag, [8, 16): second flag
         __syncwarp();
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       // Thread 0 doubles as the TMA producer, kStages-1 slabs ahead of the math.
       auto issue = [&](int p, int stage) {
         const int K = p >> 2, sq = p & 3;
-        if (sq == 0 && j >= 8 && K > 0 && K < 256 && ((misc->ready[K >> 5] & misc->ready[8 + (K >> 5)]) >> (K & 31) & 1u)) {
+        if (sq == 0 && j >= 2 && K > 0 && K < 256 && ((misc->ready[K >> 5] & misc->ready[8 + (K >> 5)]) >> (K & 31) & 1u)) {
           fence_proxy_async_global();
         } else if (sq == 0) {
           pr.start();
