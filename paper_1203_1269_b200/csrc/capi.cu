@@ -636,6 +636,18 @@ int run_batch(gpemu_plan* pl, size_t B, bool tolerate_nonfinite = false) {
      "H2D jitter");
   for (int step = 0; step < 6 && !active.empty();) {
     const int nact = (int)active.size();
+    if (step > 0 && pl->precision == GPEMU_PRECISION_SINGLE) {
+      // In float a rung whose diagonal rounds to the previous rung's (1 + 1e-8 == 1 in float)
+      // rebuilds the same matrix: that attempt fails again by construction, so it is skipped
+      // (the recorded jitter and every value are those of the rung-by-rung ladder).
+      const float diag_base = 1.0f + (float)pl->nugget;  // kernels_f32.cu assemble
+      volatile float prev = diag_base + (float)kLadder[step - 1];
+      volatile float cur = diag_base + (float)kLadder[step];
+      if (prev == cur) {
+        ++step;
+        continue;
+      }
+    }
     if (step > 0) {
       for (int q = 0; q < nact; ++q) pl->h_jitter[active[q]] = kLadder[step];
       ck(cudaMemcpyAsync(pl->jitter.p, pl->h_jitter.data(), B * sizeof(double),

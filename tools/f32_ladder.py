@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, ".")
 import bench  # noqa: E402
 import paper_1203_1269_b200.gpemu as g  # noqa: E402
 
