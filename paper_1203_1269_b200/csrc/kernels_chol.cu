@@ -499,21 +499,28 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   // block of an L(j,j) slab (column blocks 2s, 2s+1: 15 - 4s warp blocks) is stored, the last
   // contributor releases the tile's flag as pbase + s + 1 (chain-bound OFF tasks start their
   // TRSM on the first slab; others wait for pbase + 4).
-  auto store_block = [&](int kb) {
+  auto store_block = [&](int kb) {  // the warp's finished 16x16 block of column block kb -> C
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int nsub = 0; nsub < 2; ++nsub) {
-        const int off = acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc);
-        *reinterpret_cast<double2*>(C + off) = make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
-        if (gt) __stcg(reinterpret_cast<double2*>(gt + off), make_double2(acc[mi][nsub][0], acc[mi][nsub][1]));
-      }
-    if (!gt) return;
+      for (int nsub = 0; nsub < 2; ++nsub)
+        *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
+            make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
+  };
+  // Column block kb of L(j,j) (rows 16kb..127, all final in C once every step-kb panel is in)
+  // -> HBM by the pivot warp kb after its border work, off the pivot chain; the second column
+  // block of a 32-column slab releases the slab (4 epoch + s + 1).
+  auto publish_colblock = [&](int kb) {
+    for (int q = lane; q < (8 - kb) * 128; q += 32) {  // double2 units: (8 - kb) blocks x 16 rows x 8
+      const int r = 16 * kb + (q >> 3), c2 = 2 * (q & 7);
+      const int off = elem_off(r, 16 * kb + c2);
+      __stcg(reinterpret_cast<double2*>(gt + off), *reinterpret_cast<const double2*>(C + off));
+    }
     __syncwarp();
     if (lane == 0) {
       __threadfence();
       const int sl = kb >> 1;
-      if (atomicAdd(&misc->pcnt[sl], 1) == 14 - 4 * sl) {
+      if (atomicAdd(&misc->pcnt[sl], 1) == 1) {
         fence_proxy_async_global();
         st_release_gpu(prog, pbase + sl + 1);
       }
@@ -586,6 +593,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
         __syncwarp();
         named_bar_arrive(6 + ((kb + 1) & 1), 64);
       }
+      if (gt) publish_colblock(kb);
       break;
     }
     // warp > kb: the pivot block of step kb
