@@ -68,7 +68,7 @@ __global__ void border_init_kernel(const double* __restrict__ y, int n, int Npad
 }
 
 constexpr int kAsmSlotChunk = 64;
-constexpr int kSlotILP = 8;
+constexpr int kSlotILP = 4;  // candidates per thread at a time (8: +1.5% at C3; 16 slower still)
 
 // One element per thread: its d table values stay in registers and are reused by every
 // candidate of the batch; kSlotILP candidates are processed together, branch-free (exp_neg,
