@@ -32,7 +32,7 @@ __device__ __forceinline__ double pow_abs_p(double delta, double p) { return pow
 // training rows are read by every thread at the same address (shared-memory broadcast);
 // MAXD unrolls the d pow terms so they interleave (fastmath.cuh is branch-free).
 template <int MAXD>
-__global__ void __launch_bounds__(kPredThreads, MAXD <= 12 ? 6 : 4) predict_kernel(
+__global__ void __launch_bounds__(kPredThreads, 4) predict_kernel(
     const double* __restrict__ Xt, int N, const double* __restrict__ X, int n, int d,
     const double* __restrict__ theta, double p, const double* __restrict__ alpha,
     double* __restrict__ part, int* bad) {

@@ -4,7 +4,7 @@ import sys
 import time
 import numpy as np
 import torch
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, ".")
 import paper_1203_1269_b200.gpemu as g
 n, d, N = 8192, 10, 1_000_000
 rng = np.random.default_rng(0)
