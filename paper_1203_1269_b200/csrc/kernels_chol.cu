@@ -165,8 +165,7 @@ __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers);
 __device__ __forceinline__ void wait_flag(const int* flag, int epoch, int* error) {
   if (ld_acquire_gpu(flag) == epoch) return;
   const long long t0 = clock64();
-  while (ld_acquire_gpu(flag) != epoch) {
-    __nanosleep(64);
+  while (ld_acquire_gpu(flag) != epoch) {  // tight spin: each poll is an L2 round trip anyway
     if (clock64() - t0 > kSpinLimitCycles) {
       atomicExch(error, 1);
       return;
@@ -178,8 +177,7 @@ __device__ __forceinline__ void wait_flag(const int* flag, int epoch, int* error
 __device__ __forceinline__ void wait_flag_geq(const int* flag, int target, int* error) {
   if (ld_acquire_gpu(flag) >= target) return;
   const long long t0 = clock64();
-  while (ld_acquire_gpu(flag) < target) {
-    __nanosleep(64);
+  while (ld_acquire_gpu(flag) < target) {  // (a 64 ns back-off cost 0.4% on a B=1 evaluation)
     if (clock64() - t0 > kSpinLimitCycles) {
       atomicExch(error, 1);
       return;
