@@ -1219,8 +1219,82 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           // per-lane base plus an immediate, so the DMMAs of independent column blocks
           // interleave instead of queueing behind runtime predicates.
           const int lane_base = (lr << 5) + lc;
+          if constexpr (!kProgress) {
+            // Software-pipelined: block cb's update of the next block's columns (n-tiles w+2,
+            // w+3) goes first, then block cb+1's substitution runs with the rest of block cb's
+            // update (n-tiles w+4..15) interleaved into it, so the DMMA stream fills the
+            // substitution chain's latency instead of alternating with it. Every lane takes part
+            // in the substitution (lanes 16..31 repeat rows 0..15; only lanes < 16 store), which
+            // keeps the warp converged for the interleaved mma.sync. Per accumulator the DMMAs
+            // keep their k order, so the factor is bitwise unchanged.
+            auto lk = [&](int cb, int ks) -> const double* {
+              return Ls + ((cb >> 1) << 12) + lane_base + (((((4 * cb) + ks) & 7) ^ lr) << 2);
+            };
+            stage_out_at(acc, 0, St, lr, lc);
+            __syncwarp();
+            {
+              double xr[16];
+              load_row16(xr, St + (lane & 15) * kStageLd);
+              solve_row16p(xr, Dp, rinv);
+              if (lane < 16) store_row16(xr, St + lane * kStageLd);
+            }
+            __syncwarp();
 #pragma unroll
-          for (int cb = 0; cb < 8; ++cb) {
+            for (int cb = 0; cb < 8; ++cb) {
+              const int o = 16 * cb, w = 2 * cb;
+              double av[2][4];
+              if (cb < 7) {
+#pragma unroll
+                for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                  for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -St[(8 * mi + lr) * kStageLd + 4 * ks + lc];
+              }
+              // block cb is final: store it from St
+#pragma unroll
+              for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+                for (int nsub = 0; nsub < 2; ++nsub)
+                  __stcg(reinterpret_cast<double2*>(gtile + acc_off(16 * warp + 8 * mi + lr, w + nsub, lc)),
+                         *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc));
+              if (cb < 7) {
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                  const double* Lk = lk(cb, ks);
+#pragma unroll
+                  for (int a = w + 2; a < w + 4; ++a) {
+                    const double b = Lk[a << 8];
+                    dmma884(acc[0][a][0], acc[0][a][1], av[0][ks], b);
+                    dmma884(acc[1][a][0], acc[1][a][1], av[1][ks], b);
+                  }
+                }
+                __syncwarp();  // St (A fragments, store) read before block cb+1 overwrites it
+                stage_out_at(acc, w + 2, St, lr, lc);
+                __syncwarp();
+                double xr[16];
+                load_row16(xr, St + (lane & 15) * kStageLd);
+                const double* D = Dp + (cb + 1) * kTriElems;
+                const double* ri = rinv + o + 16;
+                const int na = 12 - w, units = 4 * na;  // (ks, a) pairs left of block cb's update
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                  xr[c] = div_by(xr[c], D[c * (c + 1) / 2 + c], ri[c]);
+#pragma unroll
+                  for (int c2 = c + 1; c2 < 16; ++c2) xr[c2] -= xr[c] * D[c2 * (c2 + 1) / 2 + c];
+#pragma unroll
+                  for (int e = (c * units) / 16; e < ((c + 1) * units) / 16; ++e) {
+                    const int ks = e / na, a = w + 4 + e % na;
+                    const double b = lk(cb, ks)[a << 8];
+                    dmma884(acc[0][a][0], acc[0][a][1], av[0][ks], b);
+                    dmma884(acc[1][a][0], acc[1][a][1], av[1][ks], b);
+                  }
+                }
+                if (lane < 16) store_row16(xr, St + lane * kStageLd);
+                __syncwarp();
+              }
+            }
+          }
+#pragma unroll
+          for (int cb = 0; cb < (kProgress ? 8 : 0); ++cb) {
             const int o = 16 * cb, w = 2 * cb;
             if constexpr (kProgress) {
               // L(j,j) slab cb/2: its load (issued once the DIAG task published it), then the
