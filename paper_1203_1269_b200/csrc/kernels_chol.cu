@@ -423,9 +423,10 @@ __device__ __forceinline__ void pivot_root(double s, double& d, double& r) {
 // rinv[0..15]. Returns false (uniform) on a failed pivot (backend.hpp:238).
 __device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int lane, double* qs) {
   double d, r;
-  double s = __shfl_sync(0xffffffffu, xr[0], 0);
+  const double s = __shfl_sync(0xffffffffu, xr[0], 0);
   bool ok = s > 0.0;  // uniform: every lane sees the same pivots
-  if (!ok) s = 1.0;   // keep the arithmetic finite after a failure; the block is discarded
+  // (after a failed pivot the arithmetic runs on with NaN / inf: the block is discarded, and
+  // keeping the compare and select off the pivot chain saves their latency every column)
   pivot_root(s, d, r);
 #pragma unroll
   for (int c = 0; c < 16; ++c) {
@@ -433,9 +434,8 @@ __device__ __forceinline__ bool potrf_row16(double (&xr)[16], double* rinv, int 
     if (lane == c) rinv[c] = r;
     xr[c] = lane > c ? q : (lane == c ? d : xr[c]);
     if (c < 15) {  // the next pivot first: it depends only on lane c+1's own quotient
-      double sn = __shfl_sync(0xffffffffu, fma(-q, q, xr[c + 1]), c + 1);
+      const double sn = __shfl_sync(0xffffffffu, fma(-q, q, xr[c + 1]), c + 1);
       ok = ok && sn > 0.0;
-      if (!ok) sn = 1.0;
       pivot_root(sn, d, r);
     }
     // column c's quotients to every lane through shared memory (one STS per lane, broadcast
