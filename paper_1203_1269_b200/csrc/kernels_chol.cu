@@ -526,28 +526,36 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   };  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
   double* Pbuf = Dbuf + 2 * 256;                                              // [2][128][16]
   double* Stw = Pbuf + 2 * TILE * 16 + warp * (16 * kStageLd);                // per warp
+  // The look-ahead warp (kb+1) carries its diagonal block into its own pivot step in the row
+  // layout (yr): no accumulator round trip between the panel solve and the pivot.
+  double yr[16];
   for (int kb = 0; kb < 8; ++kb) {
     const int o = 16 * kb;
     double* Dblk = Dbuf + (kb & 1) * 256;
     double* P = Pbuf + (kb & 1) * (TILE * 16);
     const int bd = 2 + (kb & 1), bp = 4 + (kb & 1);
     if (warp == kb) {  // factor the pivot block, release it, done with this warp's rows
-      stage_out(acc, Stw, lr, lc);
-      __syncwarp();
       double xr[16];
-      if (lane < 16) load_row16(xr, Stw + lane * kStageLd);
+      if (kb == 0) {
+        stage_out(acc, Stw, lr, lc);
+        __syncwarp();
+        load_row16(xr, Stw + (lane & 15) * kStageLd);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) xr[c] = yr[c];
+      }
       // quotient broadcast buffer: the OFF-TRSM staging area, idle during DIAG tasks
       const bool okw = potrf_row16(xr, rinvD + o, lane,
                                    reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * 32);
       if (!okw && lane == 0) misc->fail = 1;
-      if (lane < 16) {
-        store_row16(xr, Stw + lane * kStageLd);
-        store_row16(xr, Dblk + lane * 16);
-      }
+      if (lane < 16) store_row16(xr, Dblk + lane * 16);
       __syncwarp();
-      stage_in(acc, Stw, lr, lc);
       if (kb < 7) named_bar_arrive(bd, 32 * (8 - kb));
-      store_block(kb);
+      if (lane < 16) {  // the finished block -> C
+#pragma unroll
+        for (int c = 0; c < 16; c += 2)
+          *reinterpret_cast<double2*>(C + elem_off(o + lane, o + c)) = make_double2(xr[c], xr[c + 1]);
+      }
       lap(PR_P_PIV);
       // The border rows W = [w_u; w_v] (2 x 128) ride along as two rows below the tile: the
       // pivot warp, idle after its factorization, solves their block kb against D_kb (lanes
@@ -561,10 +569,10 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       // above and BP / BB(kb+1) are not entered by anyone, so the barriers stay balanced.
       if (!okw) break;
       if (lane < 2) {
-        double xr[16];
-        load_row16(xr, W + lane * TILE + o);
-        solve_row16(xr, Dblk, rinvD + o);
-        store_row16(xr, W + lane * TILE + o);
+        double xb[16];
+        load_row16(xb, W + lane * TILE + o);
+        solve_row16(xb, Dblk, rinvD + o);
+        store_row16(xb, W + lane * TILE + o);
       }
       __syncwarp();
       // block kb of [u_j; v_j] is final: to HBM; after the odd block of a 32-column slab the
@@ -600,28 +608,54 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
     stage_out(acc, Stw, lr, lc);
     __syncwarp();
+    double xr[16];
+    load_row16(xr, Stw + (lane & 15) * kStageLd);
+    solve_row16(xr, Dblk, rinvD + o);
     if (lane < 16) {
-      double xr[16];
-      load_row16(xr, Stw + lane * kStageLd);
-      solve_row16(xr, Dblk, rinvD + o);
-      store_row16(xr, Stw + lane * kStageLd);
       const int r = 16 * warp + lane;
 #pragma unroll
-      for (int c = 0; c < 16; c += 2)
+      for (int c = 0; c < 16; c += 2) {
         *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
+        *reinterpret_cast<double2*>(C + elem_off(r, o + c)) = make_double2(xr[c], xr[c + 1]);
+      }
     }
     __syncwarp();
-    stage_in(acc, Stw, lr, lc);
-    store_block(kb);
     lap(PR_P_PANEL);
-    // BP(kb): warps kb+1..7 and the border-owning pivot warp kb
     if (warp == kb + 1) {
-      named_bar_arrive(bp, 32 * (8 - kb));  // own panel rows are in P (the next warp's look-ahead
-                                            // needs only its own rows: nlast = 3 below)
-    } else {
-      named_bar_sync(bp, 32 * (8 - kb));    // every step-kb panel is in P
+      // BP(kb): own panel rows are in P (the look-ahead needs only its own rows)
+      named_bar_arrive(bp, 32 * (8 - kb));
+      lap(PR_P_BPW);
+      // Its diagonal block (accumulator n-tiles 2, 3) -= panel * panel^T by DMMA, the A
+      // fragments straight from its own rows in P (no window reload, no quad shuffles, no
+      // window rotation: the warp's remaining columns are above the diagonal); the block then
+      // goes to the row layout for its pivot step.
+      double av[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -P[p_off(16 * warp + 8 * mi + lr, 4 * ks + lc)];
+#pragma unroll
+      for (int nb = 2; nb < 4; ++nb) {
+        const int prow = o + 8 * nb + lr;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const double b = P[p_off(prow, 4 * ks + lc)];
+          dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
+          dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
+        }
+      }
+      stage_out_at(acc, 2, Stw, lr, lc);
+      __syncwarp();
+      load_row16(yr, Stw + (lane & 15) * kStageLd);
+      lap(PR_P_UPD);
+      continue;
     }
+    named_bar_sync(bp, 32 * (8 - kb));    // every step-kb panel is in P
     lap(PR_P_BPW);
+    // the solved panel back into the accumulator window for the A fragments
+    if (lane < 16) store_row16(xr, Stw + lane * kStageLd);
+    __syncwarp();
+    stage_in(acc, Stw, lr, lc);
     double av[2][4];
     window_afrags(acc, av, lane);
     const int nlast = 2 * (warp - kb) + 1;  // the warp's own diagonal block
