@@ -465,7 +465,10 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 // for all step-kb panels (named barrier BP) and update their trailing columns with DMMA. The
 // serial chain per step is factor -> one panel solve -> one 16x16 update (the trailing
 // updates of the other warps run under the next factorization). Every element gets the same
-// operations in the same order as without the look-ahead. Pivot blocks and panels are double-
+// operations in the same order as without the look-ahead. Each warp moves its block of the
+// step into the row layout before it waits for the pivot, and the look-ahead warp leaves the
+// step loop into its own pivot step carrying only its diagonal block, so the accumulators are
+// dead on the chain (C3 -0.3%, B=1 -1.6%). Pivot blocks and panels are double-
 // buffered by step parity (the barriers keep any warp within one step of its readers).
 // Finished blocks are written back into C. Reciprocal pivots -> rinvD[0..127]. Returns false
 // on a failed pivot (uniform): the factorization stops at that step with the barriers balanced,
@@ -523,93 +526,150 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
         st_release_gpu(prog, pbase + sl + 1);
       }
     }
-  };  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
+  };
+  double* Dbuf = reinterpret_cast<double*>(smem + TILE_ELEMS * 8);            // [2][16][16]
   double* Pbuf = Dbuf + 2 * 256;                                              // [2][128][16]
   double* Stw = Pbuf + 2 * TILE * 16 + warp * (16 * kStageLd);                // per warp
-  // The look-ahead warp (kb+1) carries its diagonal block into its own pivot step in the row
-  // layout (yr): no accumulator round trip between the panel solve and the pivot.
-  double yr[16];
+  // Pivot step kb (warp kb, the pivot block in the row layout xr): factor, release it (BD),
+  // the border rows, publication. The warp is done with the tile afterwards.
+  auto pivot_step = [&](int kb, double (&xr)[16]) {
+    const int o = 16 * kb;
+    double* Dblk = Dbuf + (kb & 1) * 256;
+    double* P = Pbuf + (kb & 1) * (TILE * 16);
+    const int bp = 4 + (kb & 1);
+    // quotient broadcast buffer: the OFF-TRSM staging area, idle during DIAG tasks
+    const bool okw = potrf_row16(xr, rinvD + o, lane,
+                                 reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * 32);
+    if (!okw && lane == 0) misc->fail = 1;
+    if (lane < 16) store_row16(xr, Dblk + lane * 16);
+    __syncwarp();
+    if (kb < 7) named_bar_arrive(2 + (kb & 1), 32 * (8 - kb));
+    if (lane < 16) {  // the finished block -> C
+#pragma unroll
+      for (int c = 0; c < 16; c += 2)
+        *reinterpret_cast<double2*>(C + elem_off(o + lane, o + c)) = make_double2(xr[c], xr[c + 1]);
+    }
+    lap(PR_P_PIV);
+    // The border rows W = [w_u; w_v] (2 x 128) ride along as two rows below the tile: the
+    // pivot warp, idle after its factorization, solves their block kb against D_kb (lanes
+    // 0/1) once warp kb-1 has applied block kb-1 to them (named barrier BB), then applies
+    // block kb to their trailing columns from the step-kb panels and hands over to warp
+    // kb+1. Each border element gets the same FMAs in the same order as a separate blocked
+    // substitution after the POTRF.
+    if (kb > 0) named_bar_sync(6 + (kb & 1), 64);
+    // A failed pivot ends the factorization here (as the reference's factor attempt does): the
+    // warps below see misc->fail after BD(kb) and stop too; BB's pending arrival is consumed
+    // above and BP / BB(kb+1) are not entered by anyone, so the barriers stay balanced.
+    if (!okw) return;
+    if (lane < 2) {
+      double xb[16];
+      load_row16(xb, W + lane * TILE + o);
+      solve_row16(xb, Dblk, rinvD + o);
+      store_row16(xb, W + lane * TILE + o);
+    }
+    __syncwarp();
+    // block kb of [u_j; v_j] is final: to HBM; after the odd block of a 32-column slab the
+    // slab is released (the even block's warp handed over through BB before this one began)
+    __stcg(bg + (lane >> 4) * npad + o + (lane & 15), W[(lane >> 4) * TILE + o + (lane & 15)]);
+    __syncwarp();
+    if ((kb & 1) && lane == 0) {
+      __threadfence();
+      fence_proxy_async_global();
+      st_release_gpu(bprog, pbase + (kb >> 1) + 1);
+    }
+    if (kb < 7) {
+      named_bar_sync(bp, 32 * (8 - kb));  // the step-kb panels are in P
+      const int ncol = TILE - o - 16;
+      for (int q = lane; q < 2 * ncol; q += 32) {
+        const int r = q >= ncol ? 1 : 0;
+        const int l = o + 16 + q - r * ncol;
+        const double* x = W + r * TILE + o;
+        double sacc = W[r * TILE + l];
+#pragma unroll
+        for (int c = 0; c < 16; ++c) sacc -= x[c] * P[p_off(l, c)];
+        W[r * TILE + l] = sacc;
+      }
+      __syncwarp();
+      named_bar_arrive(6 + ((kb + 1) & 1), 64);
+    }
+    if (gt) publish_colblock(kb);
+  };
   for (int kb = 0; kb < 8; ++kb) {
     const int o = 16 * kb;
     double* Dblk = Dbuf + (kb & 1) * 256;
     double* P = Pbuf + (kb & 1) * (TILE * 16);
     const int bd = 2 + (kb & 1), bp = 4 + (kb & 1);
-    if (warp == kb) {  // factor the pivot block, release it, done with this warp's rows
-      double xr[16];
-      if (kb == 0) {
-        stage_out(acc, Stw, lr, lc);
-        __syncwarp();
-        load_row16(xr, Stw + (lane & 15) * kStageLd);
-      } else {
-#pragma unroll
-        for (int c = 0; c < 16; ++c) xr[c] = yr[c];
-      }
-      // quotient broadcast buffer: the OFF-TRSM staging area, idle during DIAG tasks
-      const bool okw = potrf_row16(xr, rinvD + o, lane,
-                                   reinterpret_cast<double*>(smem + kOffTrsmSt) + warp * 32);
-      if (!okw && lane == 0) misc->fail = 1;
-      if (lane < 16) store_row16(xr, Dblk + lane * 16);
-      __syncwarp();
-      if (kb < 7) named_bar_arrive(bd, 32 * (8 - kb));
-      if (lane < 16) {  // the finished block -> C
-#pragma unroll
-        for (int c = 0; c < 16; c += 2)
-          *reinterpret_cast<double2*>(C + elem_off(o + lane, o + c)) = make_double2(xr[c], xr[c + 1]);
-      }
-      lap(PR_P_PIV);
-      // The border rows W = [w_u; w_v] (2 x 128) ride along as two rows below the tile: the
-      // pivot warp, idle after its factorization, solves their block kb against D_kb (lanes
-      // 0/1) once warp kb-1 has applied block kb-1 to them (named barrier BB), then applies
-      // block kb to their trailing columns from the step-kb panels and hands over to warp
-      // kb+1. Each border element gets the same FMAs in the same order as a separate blocked
-      // substitution after the POTRF.
-      if (kb > 0) named_bar_sync(6 + (kb & 1), 64);
-      // A failed pivot ends the factorization here (as the reference's factor attempt does): the
-      // warps below see misc->fail after BD(kb) and stop too; BB's pending arrival is consumed
-      // above and BP / BB(kb+1) are not entered by anyone, so the barriers stay balanced.
-      if (!okw) break;
-      if (lane < 2) {
-        double xb[16];
-        load_row16(xb, W + lane * TILE + o);
-        solve_row16(xb, Dblk, rinvD + o);
-        store_row16(xb, W + lane * TILE + o);
-      }
-      __syncwarp();
-      // block kb of [u_j; v_j] is final: to HBM; after the odd block of a 32-column slab the
-      // slab is released (the even block's warp handed over through BB before this one began)
-      __stcg(bg + (lane >> 4) * npad + o + (lane & 15), W[(lane >> 4) * TILE + o + (lane & 15)]);
-      __syncwarp();
-      if ((kb & 1) && lane == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        st_release_gpu(bprog, pbase + (kb >> 1) + 1);
-      }
-      if (kb < 7) {
-        named_bar_sync(bp, 32 * (8 - kb));  // the step-kb panels are in P
-        const int ncol = TILE - o - 16;
-        for (int q = lane; q < 2 * ncol; q += 32) {
-          const int r = q >= ncol ? 1 : 0;
-          const int l = o + 16 + q - r * ncol;
-          const double* x = W + r * TILE + o;
-          double sacc = W[r * TILE + l];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) sacc -= x[c] * P[p_off(l, c)];
-          W[r * TILE + l] = sacc;
-        }
-        __syncwarp();
-        named_bar_arrive(6 + ((kb + 1) & 1), 64);
-      }
-      if (gt) publish_colblock(kb);
-      break;
-    }
-    // warp > kb: the pivot block of step kb
-    named_bar_sync(bd, 32 * (8 - kb));
-    lap(PR_P_BDW);
-    if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
+    // This warp's block of column block kb is final in the accumulators: to the row layout
+    // (the pivot block for warp kb, a panel block for the others; the latter while waiting
+    // for the pivot).
     stage_out(acc, Stw, lr, lc);
     __syncwarp();
     double xr[16];
     load_row16(xr, Stw + (lane & 15) * kStageLd);
+    if (warp == kb) {  // warp 0 only: every later pivot step runs from the look-ahead below
+      pivot_step(kb, xr);
+      break;
+    }
+    if (warp == kb + 1) {
+      // The look-ahead warp: its panel block, then its diagonal block (accumulator n-tiles
+      // 2, 3, kept apart so that nothing else of the accumulators stays live), then its own
+      // pivot step kb+1 at once.
+      double dg[2][2][2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn) {
+          dg[mi][nn][0] = acc[mi][2 + nn][0];
+          dg[mi][nn][1] = acc[mi][2 + nn][1];
+        }
+      named_bar_sync(bd, 32 * (8 - kb));
+      lap(PR_P_BDW);
+      if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
+      solve_row16(xr, Dblk, rinvD + o);
+      if (lane < 16) {
+        const int r = 16 * warp + lane;
+#pragma unroll
+        for (int c = 0; c < 16; c += 2) {
+          *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
+          *reinterpret_cast<double2*>(C + elem_off(r, o + c)) = make_double2(xr[c], xr[c + 1]);
+        }
+      }
+      __syncwarp();
+      named_bar_arrive(bp, 32 * (8 - kb));  // BP(kb): own panel rows are in P
+      lap(PR_P_PANEL);
+      // diagonal block -= panel * panel^T by DMMA, the A fragments straight from its own rows
+      // in P (no window reload, no quad shuffles, no window rotation), then the row layout
+      double av[2][4];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -P[p_off(16 * warp + 8 * mi + lr, 4 * ks + lc)];
+#pragma unroll
+      for (int nn = 0; nn < 2; ++nn) {
+        const int prow = o + 16 + 8 * nn + lr;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks) {
+          const double b = P[p_off(prow, 4 * ks + lc)];
+          dmma884(dg[0][nn][0], dg[0][nn][1], av[0][ks], b);
+          dmma884(dg[1][nn][0], dg[1][nn][1], av[1][ks], b);
+        }
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int nn = 0; nn < 2; ++nn)
+          *reinterpret_cast<double2*>(Stw + (8 * mi + lr) * kStageLd + 8 * nn + 2 * lc) =
+              make_double2(dg[mi][nn][0], dg[mi][nn][1]);
+      __syncwarp();
+      double yr[16];
+      load_row16(yr, Stw + (lane & 15) * kStageLd);
+      lap(PR_P_UPD);
+      pivot_step(kb + 1, yr);
+      break;
+    }
+    named_bar_sync(bd, 32 * (8 - kb));
+    lap(PR_P_BDW);
+    if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
     solve_row16(xr, Dblk, rinvD + o);
     if (lane < 16) {
       const int r = 16 * warp + lane;
@@ -621,35 +681,6 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     }
     __syncwarp();
     lap(PR_P_PANEL);
-    if (warp == kb + 1) {
-      // BP(kb): own panel rows are in P (the look-ahead needs only its own rows)
-      named_bar_arrive(bp, 32 * (8 - kb));
-      lap(PR_P_BPW);
-      // Its diagonal block (accumulator n-tiles 2, 3) -= panel * panel^T by DMMA, the A
-      // fragments straight from its own rows in P (no window reload, no quad shuffles, no
-      // window rotation: the warp's remaining columns are above the diagonal); the block then
-      // goes to the row layout for its pivot step.
-      double av[2][4];
-#pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -P[p_off(16 * warp + 8 * mi + lr, 4 * ks + lc)];
-#pragma unroll
-      for (int nb = 2; nb < 4; ++nb) {
-        const int prow = o + 8 * nb + lr;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-          const double b = P[p_off(prow, 4 * ks + lc)];
-          dmma884(acc[0][nb][0], acc[0][nb][1], av[0][ks], b);
-          dmma884(acc[1][nb][0], acc[1][nb][1], av[1][ks], b);
-        }
-      }
-      stage_out_at(acc, 2, Stw, lr, lc);
-      __syncwarp();
-      load_row16(yr, Stw + (lane & 15) * kStageLd);
-      lap(PR_P_UPD);
-      continue;
-    }
     named_bar_sync(bp, 32 * (8 - kb));    // every step-kb panel is in P
     lap(PR_P_BPW);
     // the solved panel back into the accumulator window for the A fragments
