@@ -468,7 +468,9 @@ __device__ __forceinline__ double& Cs(double* C, int r, int c) { return C[elem_o
 // operations in the same order as without the look-ahead. Each warp moves its block of the
 // step into the row layout before it waits for the pivot, and the look-ahead warp leaves the
 // step loop into its own pivot step carrying only its diagonal block, so the accumulators are
-// dead on the chain (C3 -0.3%, B=1 -1.6%). Pivot blocks and panels are double-
+// dead on the chain (C3 -0.3%, B=1 -1.6%). BD is split: the look-ahead warp waits only for
+// the pivot (named barrier 8/9), the warps below it on their own barrier. Pivot blocks and
+// panels are double-
 // buffered by step parity (the barriers keep any warp within one step of its readers).
 // Finished blocks are written back into C. Reciprocal pivots -> rinvD[0..127]. Returns false
 // on a failed pivot (uniform): the factorization stops at that step with the barriers balanced,
@@ -477,6 +479,11 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
                                         int warp, int lane, unsigned long long* pp, double* gt, int* prog,
                                         int pbase, double* bg, int npad, int* bprog) {
   const int lr = lane >> 2, lc = lane & 3;
+  // Row block of this warp: blocks 2i and 2i+1 on warps i and i+4, i.e. on the same SM
+  // sub-partition (warp w issues from SMSP w % 4). The pivot of step kb then shares its
+  // sub-partition's FP64 pipe only with the look-ahead warp (waiting) or a finished one, never
+  // with a warp streaming the trailing-update DMMAs.
+  const int rb = 2 * (warp & 3) + (warp >> 2);
 
   // optional per-phase cycle counters (diagnostics; pp = this CTA's counters or null)
   long long tprev = pp ? clock64() : 0;
@@ -492,7 +499,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 16; ++ni) {
-      const double2 v = *reinterpret_cast<const double2*>(C + acc_off(16 * warp + 8 * mi + lr, ni, lc));
+      const double2 v = *reinterpret_cast<const double2*>(C + acc_off(16 * rb + 8 * mi + lr, ni, lc));
       acc[mi][ni][0] = v.x;
       acc[mi][ni][1] = v.y;
     }
@@ -500,14 +507,6 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
   // block of an L(j,j) slab (column blocks 2s, 2s+1: 15 - 4s warp blocks) is stored, the last
   // contributor releases the tile's flag as pbase + s + 1 (chain-bound OFF tasks start their
   // TRSM on the first slab; others wait for pbase + 4).
-  auto store_block = [&](int kb) {  // the warp's finished 16x16 block of column block kb -> C
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-      for (int nsub = 0; nsub < 2; ++nsub)
-        *reinterpret_cast<double2*>(C + acc_off(16 * warp + 8 * mi + lr, 2 * kb + nsub, lc)) =
-            make_double2(acc[mi][nsub][0], acc[mi][nsub][1]);
-  };
   // Column block kb of L(j,j) (rows 16kb..127, all final in C once every step-kb panel is in)
   // -> HBM by the pivot warp kb after its border work, off the pivot chain; the second column
   // block of a 32-column slab releases the slab (4 epoch + s + 1).
@@ -543,7 +542,10 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     if (!okw && lane == 0) misc->fail = 1;
     if (lane < 16) store_row16(xr, Dblk + lane * 16);
     __syncwarp();
-    if (kb < 7) named_bar_arrive(2 + (kb & 1), 32 * (8 - kb));
+    // BD(kb) in two parts: the look-ahead warp alone (the chain), the warps below it (their
+    // panels; they may still be finishing the previous step's trailing update)
+    if (kb < 7) named_bar_arrive(8 + (kb & 1), 64);
+    if (kb < 6) named_bar_arrive(2 + (kb & 1), 32 * (7 - kb));
     if (lane < 16) {  // the finished block -> C
 #pragma unroll
       for (int c = 0; c < 16; c += 2)
@@ -606,11 +608,11 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     __syncwarp();
     double xr[16];
     load_row16(xr, Stw + (lane & 15) * kStageLd);
-    if (warp == kb) {  // warp 0 only: every later pivot step runs from the look-ahead below
+    if (rb == kb) {  // block 0 only: every later pivot step runs from the look-ahead below
       pivot_step(kb, xr);
       break;
     }
-    if (warp == kb + 1) {
+    if (rb == kb + 1) {
       // The look-ahead warp: its panel block, then its diagonal block (accumulator n-tiles
       // 2, 3, kept apart so that nothing else of the accumulators stays live), then its own
       // pivot step kb+1 at once.
@@ -622,12 +624,12 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
           dg[mi][nn][0] = acc[mi][2 + nn][0];
           dg[mi][nn][1] = acc[mi][2 + nn][1];
         }
-      named_bar_sync(bd, 32 * (8 - kb));
+      named_bar_sync(8 + (kb & 1), 64);
       lap(PR_P_BDW);
       if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
       solve_row16(xr, Dblk, rinvD + o);
       if (lane < 16) {
-        const int r = 16 * warp + lane;
+        const int r = 16 * rb + lane;
 #pragma unroll
         for (int c = 0; c < 16; c += 2) {
           *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
@@ -643,7 +645,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -P[p_off(16 * warp + 8 * mi + lr, 4 * ks + lc)];
+        for (int ks = 0; ks < 4; ++ks) av[mi][ks] = -P[p_off(16 * rb + 8 * mi + lr, 4 * ks + lc)];
 #pragma unroll
       for (int nn = 0; nn < 2; ++nn) {
         const int prow = o + 16 + 8 * nn + lr;
@@ -667,12 +669,12 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
       pivot_step(kb + 1, yr);
       break;
     }
-    named_bar_sync(bd, 32 * (8 - kb));
+    named_bar_sync(bd, 32 * (7 - kb));
     lap(PR_P_BDW);
     if (misc->fail) break;  // the pivot failed: the candidate climbs the jitter ladder
     solve_row16(xr, Dblk, rinvD + o);
     if (lane < 16) {
-      const int r = 16 * warp + lane;
+      const int r = 16 * rb + lane;
 #pragma unroll
       for (int c = 0; c < 16; c += 2) {
         *reinterpret_cast<double2*>(P + p_off(r, c)) = make_double2(xr[c], xr[c + 1]);
@@ -689,7 +691,7 @@ __device__ __noinline__ bool diag_potrf(unsigned char* smem, double* C, double* 
     stage_in(acc, Stw, lr, lc);
     double av[2][4];
     window_afrags(acc, av, lane);
-    const int nlast = 2 * (warp - kb) + 1;  // the warp's own diagonal block
+    const int nlast = 2 * (rb - kb) + 1;  // the warp's own diagonal block
 #pragma unroll
     for (int nb = 2; nb < 16; ++nb) {
       if (nb <= nlast) {
