@@ -157,7 +157,10 @@ struct Misc {  // per-task scalars in shared memory (kept out of the mainloop's 
   int run;             // OFF task: the candidate was still unfailed at the TRSM start
   int pcnt[4];         // DIAG: warp blocks of each L(j,j) slab stored (progressive publication)
   int ljj_issued;      // OFF (chain-bound launches): L(j,j) slabs whose loads are issued
+  int freed[3];        // DIAG (chain-bound): slab + 1 whose ring stage's refill was decided
+  int pend[3];         // ... and was deferred (its progress flags were not yet published)
 };
+static_assert(sizeof(Misc) <= 160, "Misc overlaps the TRSM staging area");
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(1, kConsumers); }
 
@@ -941,7 +944,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (ext) {
             f = &a.ext_flags[(size_t)It * NT + K];
           } else if (part == 0) {
-            f = (slab_progress && diag && K == j - 1) ? nullptr : &flags[j * NT + K];
+            f = (slab_progress && K == j - 1) ? nullptr : &flags[j * NT + K];
           } else {
             f = diag ? &flags[NT * NT + K] : &flags[I * NT + K];
           }
@@ -954,8 +957,20 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       }
 
       // Thread 0 doubles as the TMA producer, kStages-1 slabs ahead of the math.
-      auto issue = [&](int p, int stage) {
+      auto issue = [&](int p, int stage, bool may_defer) {
         const int K = p >> 2, sq = p & 3;
+        // progress word of this task's other operand of the last K-tile: the border segment
+        // (DIAG) or L(I, j-1) (OFF)
+        const int* pw2 = diag ? &flags[NT * NT + K] : &flags[(j - 1) * NT + I];
+        if (slab_progress && K == j - 1 && may_defer) {
+          // A slab of the last K-tile whose progress flags are not yet published is not
+          // waited for here (the issuing warp would sit on the flag with its own math for the
+          // slabs in between undone): thread 0 issues it when the math reaches it.
+          if (ld_acquire_gpu(&flags[(j - 1) * NT + j]) < 4 * epoch + sq + 1 || ld_acquire_gpu(pw2) < 4 * epoch + sq + 1) {
+            misc->pend[stage] = p + 1;
+            return;
+          }
+        }
         if (sq == 0 && j >= 2 && K > 0 && K < 256 && ((misc->ready[K >> 5] & misc->ready[8 + (K >> 5)]) >> (K & 31) & 1u)) {
           fence_proxy_async_global();
         } else if (sq == 0) {
@@ -964,11 +979,13 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           if (ext) {
             wait_flag(&a.ext_flags[(size_t)It * NT + K], epoch, a.error);
           } else {
-            if (!(slab_progress && diag && K == j - 1)) wait_flag(&flags[j * NT + K], epoch, a.error);
-            if (diag) {  // border rows of column K (progressive: 4 epoch + slabs done)
-              if (!(slab_progress && K == j - 1)) wait_flag_geq(&flags[NT * NT + K], 4 * epoch + 4, a.error);
-            } else {
-              wait_flag(&flags[I * NT + K], epoch, a.error);
+            if (!(slab_progress && K == j - 1)) {
+              wait_flag(&flags[j * NT + K], epoch, a.error);
+              if (diag) {  // border rows of column K (progressive: 4 epoch + slabs done)
+                wait_flag_geq(&flags[NT * NT + K], 4 * epoch + 4, a.error);
+              } else {
+                wait_flag(&flags[I * NT + K], epoch, a.error);
+              }
             }
           }
           fence_proxy_async_global();
@@ -976,11 +993,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
                                 (unsigned long long)(clock64() - tw0));
           pr.lap(PR_PROD_FLAGS);
         }
-        if (slab_progress && diag && K == j - 1) {
-          // the sub-diagonal tile L(j, j-1) is consumed slab by slab as its OFF task's TRSM
-          // finishes them: progress word flags[(j-1)*NT + j] = 4*epoch + slabs done
+        if (slab_progress && K == j - 1) {
+          // the last K-tile is consumed slab by slab as the OFF tasks' TRSMs of column j-1
+          // finish them: L(j, j-1) through the progress word flags[(j-1)*NT + j] = 4*epoch +
+          // slabs done, and the border segment (DIAG) or L(I, j-1) (OFF, word flags[(j-1)*NT + I])
           wait_flag_geq(&flags[(j - 1) * NT + j], 4 * epoch + sq + 1, a.error);
-          wait_flag_geq(&flags[NT * NT + K], 4 * epoch + sq + 1, a.error);  // and its border segment
+          wait_flag_geq(pw2, 4 * epoch + sq + 1, a.error);
           fence_proxy_async_global();
         }
         unsigned char* dst = smem + kOffStages + stage * kStageBytes;
@@ -1003,7 +1021,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
       if (pre) cur = 2;
       if (tid == 0) {
         const long long tsave = pr.last;
-        for (int p = pre; p < kStages && p < nslab; ++p) issue(p, cur + p < kStages ? cur + p : cur + p - kStages);
+        if constexpr (slab_progress) {
+#pragma unroll
+          for (int st = 0; st < kStages; ++st) misc->freed[st] = misc->pend[st] = 0;
+          if (pre) misc->freed[2] = 1;
+        }
+        for (int p = pre; p < kStages && p < nslab; ++p) {
+          const int st = cur + p < kStages ? cur + p : cur + p - kStages;
+          issue(p, st, true);
+          if constexpr (slab_progress) misc->freed[st] = p + 1;
+        }
+        if constexpr (slab_progress) __threadfence_block();
         pr.last = tsave;
       }
       for (int q = 0; q < nslab; ++q) {
@@ -1011,6 +1039,17 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         cur = cur == kStages - 1 ? 0 : cur + 1;
         const uint32_t par = (ph >> stage) & 1u;
         ph ^= 1u << stage;
+        if (slab_progress && tid == 0 && q >= SLABS_PER_TILE * (j - 1)) {
+          // a deferred slab of the last K-tile: once its stage's refill was decided, wait for
+          // its flags and issue it now
+          while (*((volatile int*)&misc->freed[stage]) != q + 1) {
+          }
+          if (*((volatile int*)&misc->pend[stage]) == q + 1) {
+            const long long tsave = pr.last;
+            issue(q, stage, false);
+            pr.last = tsave;
+          }
+        }
         if (tid == 0 && pr.p) {
           const long long tw = clock64();
           mbar_wait(&full[stage], par);
@@ -1104,8 +1143,12 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
             if (q + kStages < nslab) {
               fence_proxy_async_shared();  // generic-proxy reads of the stage before the TMA write
               const long long tsave = pr.last;
-              issue(q + kStages, stage);
+              issue(q + kStages, stage, true);
               pr.last = tsave;
+              if constexpr (slab_progress) {
+                __threadfence_block();
+                *((volatile int*)&misc->freed[stage]) = q + kStages + 1;
+              }
             }
           }
         }
@@ -1246,7 +1289,9 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
         }
       } else {
         // ------------------------------ OFF -------------------------------
-        const bool sub = slab_progress && I == j + 1;  // feeds DIAG(j+1)'s last k-step
+        // chain-bound launches release every OFF tile slab by slab (progress word flags[j*NT + I],
+        // the unused upper half): the last k-steps of DIAG(I) / OFF(I', I) consume them as they come
+        const bool sub = slab_progress;
         // L(I,j) = C L(j,j)^-T. L(j,j) arrives by TMA into the (now idle) stage ring;
         // each warp then solves its own 16 rows in registers, 16 columns at a time:
         // (a) in-block substitution (quad shuffles), (b) DMMA update of the columns to
@@ -1436,7 +1481,7 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
                        kProgress ? make_double2(acc[mi][w + nsub][0], acc[mi][w + nsub][1])
                                  : *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc));
             if constexpr (!kProgress) __syncwarp();  // St is rewritten by the next block
-            if (sub && (cb & 1) && cb < 7) {  // slab cb/2 of L(j+1, j) is final: release it
+            if (sub && (cb & 1) && cb < 7) {  // slab cb/2 of L(I, j) is final: release it
               consumer_sync();
               if (tid == 0) publish_flag(&flags[j * NT + I], 4 * epoch + (cb >> 1) + 1);
             }
