@@ -1331,6 +1331,10 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
           // per-lane base plus an immediate, so the DMMAs of independent column blocks
           // interleave instead of queueing behind runtime predicates.
           const int lane_base = (lr << 5) + lc;
+          if (kProgress && tid == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) misc->pcnt[q] = 0;  // slab releases (counted before the first block barrier below)
+          }
           if constexpr (!kProgress) {
             // Software-pipelined: block cb's update of the next block's columns (n-tiles w+2,
             // w+3) goes first, then block cb+1's substitution runs with the rest of block cb's
@@ -1482,8 +1486,16 @@ __global__ void __launch_bounds__(kThreads, 1) chol_dag_kernel(DagLaunch a) {
                                  : *reinterpret_cast<const double2*>(St + (8 * mi + lr) * kStageLd + 8 * nsub + 2 * lc));
             if constexpr (!kProgress) __syncwarp();  // St is rewritten by the next block
             if (sub && (cb & 1) && cb < 7) {  // slab cb/2 of L(I, j) is final: release it
-              consumer_sync();
-              if (tid == 0) publish_flag(&flags[j * NT + I], 4 * epoch + (cb >> 1) + 1);
+              // each warp fences its own stores, the last one to get there releases the slab:
+              // no block barrier, and the fences overlap the next slab's work
+              __syncwarp();
+              if (lane == 0) {
+                __threadfence();
+                if (atomicAdd(&misc->pcnt[cb >> 1], 1) == kConsumerWarps - 1) {
+                  fence_proxy_async_global();
+                  st_release_gpu(&flags[j * NT + I], 4 * epoch + (cb >> 1) + 1);
+                }
+              }
             }
           }
           if (tid == 0) pr.lap(PR_TRSM);
