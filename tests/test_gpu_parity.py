@@ -726,3 +726,34 @@ def test_ladder_invariance_across_kernel_instantiations(g, ctx):
         one = ev.eval_batch(th[i:i + 1])
         assert one["jitter"][0] == big["jitter"][i] and one["neg2"][0] == big["neg2"][i]
     ev.close()
+
+
+@pytest.mark.parametrize("seed", [5, 6])
+def test_launch_shape_invariance_random_designs(g, ctx, seed):
+    """A short run of tools/stress_dag.py's check: random designs (partial last tiles, d 1-6,
+    p in {1, 1.5, 1.95, 2}, thetas from 1e-5 to 31: many candidates fail pivots at various
+    columns) evaluated in a 100-candidate launch (throughput kernel), again, in an 8-candidate
+    launch and alone (chain-bound kernel: slab-wise release of every OFF tile, last K-tiles
+    consumed slab by slab, deferred slab issue, per-warp slab releases). Every record must
+    agree bitwise across the four launches."""
+    rng = np.random.default_rng(seed)
+    be = g.Backend(ctx)
+    for _ in range(12):
+        n = int(rng.choice([257, 600, 1500, 2100]))
+        d = int(rng.integers(1, 7))
+        p = float(rng.choice([1.0, 1.5, 1.95, 2.0]))
+        X = rng.random((n, d))
+        y = np.sin(3 * X).sum(1) + 0.1 * rng.standard_normal(n)
+        th = 10 ** rng.uniform(-5.0, 1.5, size=(100, d))
+        ev = g.ProfileEvaluator(g.new_dataset(X, y), p, 0.0, be, max_batch=100)
+        a = ev.eval_batch(th)
+        b = ev.eval_batch(th)
+        lo = int(rng.integers(0, 92))
+        c = ev.eval_batch(th[lo:lo + 8])
+        i = int(rng.integers(0, 100))
+        e = ev.eval_batch(th[i:i + 1])
+        for k in ("neg2", "mu", "sigma2", "jitter", "log_det"):
+            assert np.array_equal(a[k], b[k], equal_nan=True), (n, d, p, k)
+            assert np.array_equal(a[k][lo:lo + 8], c[k], equal_nan=True), (n, d, p, lo, k)
+            assert np.array_equal(a[k][i:i + 1], e[k], equal_nan=True), (n, d, p, i, k)
+        ev.close()
