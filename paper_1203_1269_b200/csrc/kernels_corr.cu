@@ -74,7 +74,7 @@ constexpr int kSlotILP = 4;  // candidates per thread at a time (8: +1.5% at C3;
 // candidate of the batch; kSlotILP candidates are processed together, branch-free (exp_neg,
 // stores predicated), so their k-sums and exps interleave. MAXD is a compile-time bound on d
 // (dispatch below), so the k loop is fully unrolled with no dead iterations.
-template <int MAXD, bool kSplit>
+template <int MAXD, bool kSplit, int ILP = kSlotILP>
 __global__ void __launch_bounds__(256) assemble_kernel(
     const double* __restrict__ table, const double* __restrict__ theta, int n, int d,
     double nugget, int NT, const int* __restrict__ slots, int nslots,
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) assemble_kernel(
       soff[q] = (long long)slot * (long long)slot_stride;
     }
     __syncthreads();
-    const int cn_pad = (cn + kSlotILP - 1) / kSlotILP * kSlotILP;
+    const int cn_pad = (cn + ILP - 1) / ILP * ILP;
     for (int e = blockIdx.y * blockDim.x + threadIdx.x; e < TILE_ELEMS;
          e += gridDim.y * blockDim.x) {
       int r, c;
@@ -128,23 +128,27 @@ __global__ void __launch_bounds__(256) assemble_kernel(
       double t[MAXD];
 #pragma unroll
       for (int k = 0; k < MAXD; ++k) t[k] = (k < d) ? __ldg(tb + (size_t)k * TILE_ELEMS + e) : 0.0;
-      for (int s0 = 0; s0 < cn_pad; s0 += kSlotILP) {
-        double s[kSlotILP], v[kSlotILP];
+      for (int s0 = 0; s0 < cn_pad; s0 += ILP) {
+        double s[ILP], v[ILP];
 #pragma unroll
-        for (int q = 0; q < kSlotILP; ++q) s[q] = 0.0;
+        for (int q = 0; q < ILP; ++q) s[q] = 0.0;
 #pragma unroll
         for (int k = 0; k < MAXD; ++k) {
+          if constexpr (ILP == 1) {
+            s[0] = fma(th[k * kAsmSlotChunk + s0], t[k], s[0]);
+          } else {
 #pragma unroll
-          for (int q = 0; q < kSlotILP; q += 2) {
-            const double2 tq = *reinterpret_cast<const double2*>(th + k * kAsmSlotChunk + s0 + q);
-            s[q] = fma(tq.x, t[k], s[q]);
-            s[q + 1] = fma(tq.y, t[k], s[q + 1]);
+            for (int q = 0; q < ILP; q += 2) {
+              const double2 tq = *reinterpret_cast<const double2*>(th + k * kAsmSlotChunk + s0 + q);
+              s[q] = fma(tq.x, t[k], s[q]);
+              s[q + 1] = fma(tq.y, t[k], s[q + 1]);
+            }
           }
         }
 #pragma unroll
-        for (int q = 0; q < kSlotILP; ++q) v[q] = exp_neg(s[q]);
+        for (int q = 0; q < ILP; ++q) v[q] = exp_neg(s[q]);
 #pragma unroll
-        for (int q = 0; q < kSlotILP; ++q) {
+        for (int q = 0; q < ILP; ++q) {
           dst[soff[s0 + q]] = v[q];
           // GPEMU_SLOT_NONFINITE (correlation.hpp:58-61): s >= 0 for validated inputs, so exp(-s)
           // is non-finite exactly when s is NaN (exp_neg maps NaN to 0)
@@ -215,6 +219,9 @@ static void launch_asm(dim3 grid, cudaStream_t s, const double* table, const dou
   if (grid.z > 1)
     assemble_kernel<MAXD, true><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
                                                      factors, slot_stride, status, chunk);
+  else if (nslots == 1)  // one candidate (model building, B=1): no padded ILP groups of copies
+    assemble_kernel<MAXD, false, 1><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
+                                                         factors, slot_stride, status, chunk);
   else
     assemble_kernel<MAXD, false><<<grid, 256, 0, s>>>(table, theta, n, d, nugget, NT, slots, nslots, jitter,
                                                       factors, slot_stride, status, chunk);
